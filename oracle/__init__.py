@@ -1,0 +1,166 @@
+"""oracle — TEST INFRASTRUCTURE ONLY.
+
+ctypes wrapper over ``oracle/liboracle.so`` (built from ``oracle/oracle.c`` by
+plain gcc).  Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package.  It
+shares no code with the CUDA path (``paper_2202_10297_b200``) and never
+imports it; the numeric tags below are re-declared from DESIGN.md.
+
+Every function takes and returns numpy arrays on the host.  See oracle.c for
+the paper passages each function follows.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+F32, F64 = 1, 2
+I32, I64 = 1, 2
+ADD, MUL, MIN, MAX, LINREC, MAT2 = 1, 2, 3, 4, 5, 6
+OPS = {"add": ADD, "mul": MUL, "min": MIN, "max": MAX, "linrec": LINREC, "mat2": MAT2}
+WIDTH = {ADD: 1, MUL: 1, MIN: 1, MAX: 1, LINREC: 2, MAT2: 4}
+ACCUMULATE = 1
+EDUPINDEX = 5
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c into liboracle.so (gcc, -O2, no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(
+            ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fno-fast-math",
+             "-ffp-contract=off", "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        vp, i64, u32, ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint, ctypes.c_int
+        L.oracle_vjp_scan.argtypes = [ci, ci, i64, vp, vp, vp, vp, u32]
+        L.oracle_vjp_reduce.argtypes = [ci, ci, i64, vp, vp, vp, vp, vp, vp, u32]
+        L.oracle_vjp_reduce_by_index.argtypes = [ci, ci, ci, i64, i64, vp, vp, vp, vp, vp, vp, vp, u32]
+        L.oracle_vjp_scatter.argtypes = [ci, ci, i64, i64, i64, vp, vp, vp, vp, u32]
+        for f in (L.oracle_vjp_scan, L.oracle_vjp_reduce, L.oracle_vjp_reduce_by_index,
+                  L.oracle_vjp_scatter):
+            f.restype = ci
+        _lib = L
+    return _lib
+
+
+def _dt(a: np.ndarray) -> int:
+    if a.dtype == np.float32:
+        return F32
+    if a.dtype == np.float64:
+        return F64
+    raise TypeError(f"oracle: unsupported value dtype {a.dtype}")
+
+
+def _it(a: np.ndarray) -> int:
+    if a.dtype == np.int32:
+        return I32
+    if a.dtype == np.int64:
+        return I64
+    raise TypeError(f"oracle: unsupported index dtype {a.dtype}")
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _op(op) -> int:
+    return OPS[op] if isinstance(op, str) else int(op)
+
+
+def vjp_scan(op, ys_bar: np.ndarray, as_: np.ndarray | None = None, *, out=None,
+             accumulate: bool = False, want_ys: bool = False):
+    """as_bar of ys = scan op as_ with output adjoint ys_bar.
+
+    Arrays are flat, element-interleaved (LINREC: d,c; MAT2: 2x2 row-major).
+    Returns as_bar (and ys if want_ys)."""
+    o = _op(op)
+    ys_bar = np.ascontiguousarray(ys_bar)
+    dt = _dt(ys_bar)
+    w = WIDTH[o]
+    assert ys_bar.size % w == 0
+    n = ys_bar.size // w
+    if as_ is not None:
+        as_ = np.ascontiguousarray(as_, dtype=ys_bar.dtype)
+        assert as_.size == ys_bar.size
+    as_bar = np.zeros_like(ys_bar) if out is None else out
+    ys = np.empty_like(ys_bar) if (want_ys and as_ is not None) else None
+    rc = lib().oracle_vjp_scan(o, dt, n, _p(as_), _p(ys_bar), _p(as_bar), _p(ys),
+                               ACCUMULATE if accumulate else 0)
+    if rc != 0:
+        raise RuntimeError(f"oracle_vjp_scan rc={rc}")
+    return (as_bar, ys) if want_ys else as_bar
+
+
+def vjp_reduce(op, as_: np.ndarray, y_bar: float, *, out=None, accumulate: bool = False):
+    """Returns (as_bar, y, arg, zeros) for y = reduce op as_."""
+    o = _op(op)
+    as_ = np.ascontiguousarray(as_)
+    dt = _dt(as_)
+    yb = np.array([y_bar], dtype=as_.dtype)
+    y = np.zeros(1, dtype=as_.dtype)
+    arg = np.zeros(1, dtype=np.int64)
+    zeros = np.zeros(1, dtype=np.int64)
+    as_bar = np.zeros_like(as_) if out is None else out
+    rc = lib().oracle_vjp_reduce(o, dt, as_.size, _p(as_), _p(yb), _p(as_bar), _p(y), _p(arg),
+                                 _p(zeros), ACCUMULATE if accumulate else 0)
+    if rc != 0:
+        raise RuntimeError(f"oracle_vjp_reduce rc={rc}")
+    return as_bar, y[0], int(arg[0]), int(zeros[0])
+
+
+def vjp_reduce_by_index(op, inds: np.ndarray, as_: np.ndarray | None, hs_bar: np.ndarray, *,
+                        out=None, accumulate: bool = False):
+    """Returns (as_bar, hs, winners, zeros) for hs = reduce_by_index op m inds as_
+    (P:1098-1126), m = len(hs_bar)."""
+    o = _op(op)
+    inds = np.ascontiguousarray(inds)
+    hs_bar = np.ascontiguousarray(hs_bar)
+    dt = _dt(hs_bar)
+    n, m = inds.size, hs_bar.size
+    if as_ is not None:
+        as_ = np.ascontiguousarray(as_, dtype=hs_bar.dtype)
+        assert as_.size == n
+    hs = np.zeros(m, dtype=hs_bar.dtype) if as_ is not None else None
+    winners = np.zeros(m, dtype=np.int64)
+    zeros = np.zeros(m, dtype=np.int64)
+    as_bar = np.zeros(n, dtype=hs_bar.dtype) if out is None else out
+    rc = lib().oracle_vjp_reduce_by_index(o, dt, _it(inds), n, m, _p(inds), _p(as_), _p(hs_bar),
+                                          _p(as_bar), _p(hs), _p(winners), _p(zeros),
+                                          ACCUMULATE if accumulate else 0)
+    if rc != 0:
+        raise RuntimeError(f"oracle_vjp_reduce_by_index rc={rc}")
+    return as_bar, hs, winners, zeros
+
+
+def vjp_scatter(is_: np.ndarray, ys_bar: np.ndarray, *, width: int = 1, vs_out=None,
+                accumulate: bool = False, in_place: bool = False):
+    """Returns (xs_bar, vs_bar, rc) for ys = scatter xs is vs.
+    rc == EDUPINDEX flags a duplicate in-range target (precondition)."""
+    is_ = np.ascontiguousarray(is_)
+    ys_bar = np.ascontiguousarray(ys_bar)
+    dt = _dt(ys_bar)
+    n = ys_bar.size // width
+    m = is_.size
+    vs_bar = np.zeros(m * width, dtype=ys_bar.dtype) if vs_out is None else vs_out
+    xs_bar = ys_bar if in_place else np.empty_like(ys_bar)
+    rc = lib().oracle_vjp_scatter(dt, _it(is_), n, m, width, _p(is_), _p(ys_bar), _p(xs_bar),
+                                  _p(vs_bar), ACCUMULATE if accumulate else 0)
+    if rc not in (0, EDUPINDEX):
+        raise RuntimeError(f"oracle_vjp_scatter rc={rc}")
+    return xs_bar, vs_bar, rc

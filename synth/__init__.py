@@ -1,0 +1,180 @@
+"""synth — seeded synthetic inputs shared by tests, smoke() and bench.py.
+
+Holds NONE of the method's arithmetic: only a counter-based generator
+(splitmix64 of (seed, stream, global index)) and the value recipes of
+DESIGN.md "Input recipe".  Every value is a pure function of
+(seed, stream, global index), so a shard [off, off+n) of a multi-GPU run is
+bit-identical to the same slice of a 1-GPU run, and the CPU and CUDA
+generators agree bit for bit (integer ops, then exact int->float scaling and
+IEEE round-to-nearest casts only; no transcendental functions).
+
+All functions return torch tensors on ``device``.
+"""
+from __future__ import annotations
+
+import torch
+
+SEED = 2202
+_M64 = (1 << 64) - 1
+
+
+def _s64(x: int) -> int:
+    """uint64 constant -> the int64 with the same bits."""
+    x &= _M64
+    return x - (1 << 64) if x >= (1 << 63) else x
+
+
+_GOLD = _s64(0x9E3779B97F4A7C15)
+_K1 = _s64(0xBF58476D1CE4E5B9)
+_K2 = _s64(0x94D049BB133111EB)
+_KS = _s64(0xD1B54A32D192ED03)
+
+
+def _srl(x: torch.Tensor, k: int) -> torch.Tensor:
+    """logical right shift of int64 bits"""
+    return (x >> k) & ((1 << (64 - k)) - 1)
+
+
+def bits(n: int, stream: int, *, offset: int = 0, seed: int = SEED, device="cpu",
+         chunk: int = 1 << 25) -> torch.Tensor:
+    """splitmix64(base + (offset + i + 1) * golden) for i in [0, n) as int64 bits."""
+    base = _s64(seed * 0x2545F4914F6CDD1D + stream * _KS)
+    out = torch.empty(n, dtype=torch.int64, device=device)
+    for s in range(0, n, chunk):
+        e = min(n, s + chunk)
+        z = torch.arange(offset + s + 1, offset + e + 1, dtype=torch.int64, device=device)
+        z = z * _GOLD + base
+        z = (z ^ _srl(z, 30)) * _K1
+        z = (z ^ _srl(z, 27)) * _K2
+        z = z ^ _srl(z, 31)
+        out[s:e] = z
+    return out
+
+
+def uniform(n: int, stream: int, *, lo=0.0, hi=1.0, dtype=torch.float64, offset: int = 0,
+            device="cpu") -> torch.Tensor:
+    """U[lo, hi): 53 random bits (f64) or 24 (f32), exact scaling then one cast."""
+    b = bits(n, stream, offset=offset, device=device)
+    if dtype == torch.float64:
+        u = _srl(b, 11).to(torch.float64) * (2.0 ** -53)
+    else:
+        u = _srl(b, 40).to(torch.float64) * (2.0 ** -24)
+    return (lo + (hi - lo) * u).to(dtype)
+
+
+def integers(n: int, stream: int, lo: int, hi: int, *, offset: int = 0, device="cpu",
+             dtype=torch.int64) -> torch.Tensor:
+    """uniform integers in [lo, hi] (multiply-shift on 32 random bits)."""
+    b = _srl(bits(n, stream, offset=offset, device=device), 32)
+    return (lo + ((b * (hi - lo + 1)) >> 32)).to(dtype)
+
+
+# --------------------------------------------------------------------------
+# recipes; stream ids are fixed per config/array
+# --------------------------------------------------------------------------
+
+def scan_add_seed(n, *, kind="uniform", dtype=torch.float64, offset=0, device="cpu"):
+    """config 1 ybar: U(0,1) (well conditioned), 'int' = integers in [-8, 8]
+    (every summation order exact), 'signed' = U(-1, 1)."""
+    if kind == "int":
+        return integers(n, 101, -8, 8, offset=offset, device=device).to(dtype)
+    if kind == "signed":
+        return uniform(n, 102, lo=-1.0, hi=1.0, dtype=dtype, offset=offset, device=device)
+    return uniform(n, 100, dtype=dtype, offset=offset, device=device)
+
+
+def linrec_inputs(n, *, dtype=torch.float64, offset=0, device="cpu"):
+    """config 2 LINREC: element (d, c), d ~ U(0,1), c ~ U(0.5, 1) (contractive);
+    seeds (Dbar, Cbar) ~ U(0,1)^2.  AoS interleaved [d0, c0, d1, c1, ...]."""
+    d = uniform(n, 200, dtype=dtype, offset=offset, device=device)
+    c = uniform(n, 201, lo=0.5, hi=1.0, dtype=dtype, offset=offset, device=device)
+    as_ = torch.stack([d, c], 1).reshape(-1)
+    ybar = uniform(2 * n, 202, dtype=dtype, offset=2 * offset, device=device)
+    return as_, ybar
+
+
+def mat2_inputs(n, *, dtype=torch.float64, offset=0, device="cpu"):
+    """config 2 MAT2: 2x2 row-major entries ~ U(0, 0.5) (positive, spectral
+    radius < 1); seeds ~ U(0,1)^4."""
+    as_ = uniform(4 * n, 210, lo=0.0, hi=0.5, dtype=dtype, offset=4 * offset, device=device)
+    ybar = uniform(4 * n, 211, dtype=dtype, offset=4 * offset, device=device)
+    return as_, ybar
+
+
+def mul_inputs(n, *, zeros="none", dtype=torch.float32, offset=0, device="cpu", n_total=None):
+    """config 3 reduce(*): a_i = 1 + (u - 1/2) * 2^-11 (log-centred: the product
+    of 2^30 of them stays within ~e^-11..e^11 in f32 and f64).  Zero injection
+    (positions from the integer generator, independent of sharding):
+      'none' z = 0; 'one' z = 1; 'two' z = 2; 'sparse' each element zero with
+      probability 2^-20 (~1024 zeros at 2^30).  The first injected zero of
+      'one'/'two' is -0.0 (must count as a zero, IEEE)."""
+    N = n_total if n_total is not None else n + offset
+    u = uniform(n, 300, dtype=torch.float64, offset=offset, device=device)
+    a = (1.0 + (u - 0.5) * (2.0 ** -11)).to(dtype)
+    if zeros in ("one", "two"):
+        pos = [int(p) for p in integers(2, 301, 0, N - 1)]
+        if zeros == "two" and pos[1] == pos[0]:
+            pos[1] = (pos[0] + N // 2) % N
+        for k, p in enumerate(pos[: 1 if zeros == "one" else 2]):
+            if offset <= p < offset + n:
+                a[p - offset] = -0.0 if k == 0 else 0.0
+    elif zeros == "sparse":
+        b = bits(n, 302, offset=offset, device=device)
+        a[_srl(b, 44) == 0] = 0.0
+    return a
+
+
+def min_inputs(n, *, dtype=torch.float32, offset=0, device="cpu", n_total=None):
+    """config 3' reduce(min): a_i = k / 2^24, k uniform in 24 bits (about 64
+    exact ties at 0.0 for 2^30), plus 3 planted copies of -1/2^24 below every
+    other value and a (-0.0, +0.0) pair; the winner is the lowest planted index."""
+    N = n_total if n_total is not None else n + offset
+    k = integers(n, 310, 0, (1 << 24) - 1, offset=offset, device=device)
+    a = (k.to(torch.float64) * (2.0 ** -24)).to(dtype)
+    plants = [int(p) for p in integers(5, 311, 0, N - 1)]
+    for j, p in enumerate(plants):
+        if offset <= p < offset + n:
+            a[p - offset] = -(2.0 ** -24) if j < 3 else (-0.0 if j == 3 else 0.0)
+    return a
+
+
+def rbi_inputs(n, m, op, *, dtype=torch.float64, itype=torch.int32, offset=0, device="cpu",
+               skew=False):
+    """config 4 reduce_by_index, k-means shaped: bins i.i.d. uniform over m
+    (skew=True: bin = floor(m * u^2), a heavy head of small bins); h̄s ~ U(0.5, 1.5).
+    '+'/'max'/'min': values on a 2^-12 grid of U(0,1) so per-bin ties at the
+    extremum occur (lowest index must win).  '*': log-centred 1 + (u-1/2)2^-10
+    with zeros of probability ~ m/n (per-bin zero count ~ Poisson(1))."""
+    if skew:
+        u = uniform(n, 400, offset=offset, device=device)
+        inds = torch.clamp((u * u * m).floor(), max=m - 1).to(itype)
+    else:
+        inds = integers(n, 400, 0, m - 1, offset=offset, device=device, dtype=itype)
+    if op == "mul":
+        u = uniform(n, 401, offset=offset, device=device)
+        a = (1.0 + (u - 0.5) * (2.0 ** -10)).to(dtype)
+        # zero with probability m/n: compare 62 random bits against m/n * 2^62
+        thr = int(min(1.0, m / max(n, 1)) * (1 << 62))
+        b = _srl(bits(n, 402, offset=offset, device=device), 2)
+        a[b < thr] = 0.0
+    else:
+        k = integers(n, 403, 0, (1 << 12) - 1, offset=offset, device=device)
+        a = (k.to(torch.float64) * (2.0 ** -12)).to(dtype)
+    hs_bar = uniform(m, 404, lo=0.5, hi=1.5, dtype=dtype, device=device)
+    return inds, a, hs_bar
+
+
+def scatter_inputs(n, m, *, dtype=torch.float64, itype=torch.int64, device="cpu", oob=0):
+    """Distinct targets is_j = (a*j + b) mod n with gcd(a, n) = 1 (a bijection),
+    the first `oob` of them replaced by out-of-range values; ybar ~ U(-1, 1)."""
+    import math
+    a = 0x9E3779B1 % n if n > 1 else 1
+    while n > 1 and math.gcd(a, n) != 1:
+        a += 1
+    b = 12345 % n if n else 0
+    j = torch.arange(m, dtype=torch.int64, device=device)
+    is_ = (j * a + b) % n if n else j
+    if oob:
+        is_[:oob] = n + torch.arange(oob, device=device) * 7 + 1
+    ybar = uniform(n, 500, lo=-1.0, hi=1.0, dtype=dtype, device=device)
+    return is_.to(itype), ybar
