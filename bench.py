@@ -1,0 +1,308 @@
+#!/usr/bin/env python
+"""bench.py — vjp elements/s and achieved HBM GB/s on B200 (BASELINE.json metric).
+
+Default workload (BASELINE.json configs[1], the config the metric is quoted on
+for one GPU): the vjp of scan with the 2x2 linear-recurrence (LINREC) and the
+2x2 matrix-multiply (MAT2) operators, n = 2^26 elements per operator, f64.  One
+STEP = one whole pass of the hot path over one batch: vjp_scan(LINREC) then
+vjp_scan(MAT2) (forward re-execution + return sweep each).  With N GPUs each
+rank owns a contiguous 2^26-element shard of each scan (weak scaling) and the
+shards exchange their per-shard Jacobian aggregates by all_gather (the path's
+one real exchange step).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+                  [--workload config2|scan_add|reduce|rbi]
+
+Prints ONE JSON line (rank 0).  Inputs (>= 1 GiB per array) are far larger than
+the 126 MB L2, so no flush is needed between steps.  --impl reference times the
+oracle (the plain CPU definition, oracle/) on bounded samples of the same
+workload.  Other --workload values print extra lines for DESIGN.md, not the
+headline.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "vjp elements/s (scan LINREC+MAT2 n=2^26 f64 per GPU)"
+UNIT = "elements/s"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_oracle_sample(n: int, reps: int = 1):
+    """oracle (plain CPU definition, one thread) on LINREC+MAT2 samples of n elements."""
+    import oracle
+    import synth
+    a1, y1 = synth.linrec_inputs(n)
+    a2, y2 = synth.mat2_inputs(n)
+    a1, y1, a2, y2 = a1.numpy(), y1.numpy(), a2.numpy(), y2.numpy()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        oracle.vjp_scan("linrec", y1, a1)
+        oracle.vjp_scan("mat2", y2, a2)
+    dt = (time.perf_counter() - t0) / reps
+    return 2 * n / dt, dt
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    n = 1 << 22  # bounded sample per step: 2 x 2^22 elements (~1.6 s of one core)
+    times = []
+    for i in range(args.warmup + args.steps):
+        v, dt = cpu_oracle_sample(n)
+        if i >= args.warmup:
+            times.append(dt)
+    mean = statistics.mean(times)
+    val = 2 * n / mean
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (synth/, seed 2202)",
+        "config": {"workload": "vjp_scan LINREC+MAT2 f64 (bounded sample: n=2^22 per op per step)",
+                   "n_per_op": n, "ops": ["linrec", "mat2"], "parallelism": "1 CPU thread"},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"LINREC+MAT2 n=2^22 each per step, {args.steps} steps"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2202_10297_b200 as vjp
+    from paper_2202_10297_b200 import dist as vdist
+    import synth
+
+    world, rank, local = dist_env()
+    assert world == args.gpus or world == 1, "--gpus must match WORLD_SIZE"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    vjp.lib()
+
+    n = args.n or (1 << 26)
+    gN = n * world
+    off = rank * n
+    ops = ["linrec", "mat2"]
+    gens = {"linrec": synth.linrec_inputs, "mat2": synth.mat2_inputs}
+    data = {}
+    for op in ops:
+        a, yb = gens[op](n, offset=off, device=dev)
+        data[op] = (a, yb, torch.empty_like(yb))
+    torch.cuda.synchronize()
+
+    def mk():
+        return {op: {"finish_start": torch.cuda.Event(enable_timing=True),
+                     "finish_end": torch.cuda.Event(enable_timing=True)} for op in ops}
+
+    def step(evs=None):
+        for op in ops:
+            a, yb, ab = data[op]
+            vdist.scan(op, yb, a, offset=off, global_n=gN, out=ab, events=evs[op] if evs else None)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # --- timed region (device time, CUDA events on the launching stream) ---
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kev = [mk() for _ in range(args.steps)]
+    launches0 = vjp.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            starts[i].record()
+            step(kev[i])
+            ends[i].record()
+        torch.cuda.synchronize()
+    k_mat2 = [e["mat2"]["finish_start"].elapsed_time(e["mat2"]["finish_end"]) for e in kev]
+    k_lin = [e["linrec"]["finish_start"].elapsed_time(e["linrec"]["finish_end"]) for e in kev]
+    launches = vjp.launch_count() - launches0
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    mean_ms = statistics.mean(step_ms)
+    t = torch.tensor([mean_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    mean_ms = float(t.item())
+
+    # --- end to end through the public API with host buffers ---
+    e2e = None
+    if not args.no_e2e:
+        host = {}
+        for op in ops:
+            a, yb, ab = data[op]
+            host[op] = (a.cpu().pin_memory(), yb.cpu().pin_memory(), torch.empty(ab.shape, dtype=ab.dtype,
+                                                                                  pin_memory=True))
+        h2d = sum(h[0].numel() * h[0].element_size() + h[1].numel() * h[1].element_size() for h in host.values())
+        d2h = sum(h[2].numel() * h[2].element_size() for h in host.values())
+        e2e_steps = max(1, min(3, args.steps))
+        for op in ops:  # warm
+            vjp.scan(op, host[op][1], host[op][0], out=host[op][2])
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            for op in ops:
+                if world > 1:
+                    a_d = host[op][0].to(dev, non_blocking=True)
+                    y_d = host[op][1].to(dev, non_blocking=True)
+                    ab_d = vdist.scan(op, y_d, a_d, offset=off, global_n=gN)
+                    host[op][2].copy_(ab_d, non_blocking=True)
+                    torch.cuda.synchronize()
+                else:
+                    vjp.scan(op, host[op][1], host[op][0], out=host[op][2])
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_s = float(te.item())
+        e2e = {"value": 2 * gN / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": e2e_s * 1e3, "steps": e2e_steps}
+
+    if rank == 0:
+        peak, peak_src = peaks()
+        kmat2 = statistics.mean(k_mat2)
+        alg_bytes = 96 * n  # MAT2 return sweep: read A 32 B + ybar 32 B, write abar 32 B per element
+        achieved = alg_bytes / (kmat2 * 1e-3) / 1e9
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(prof):
+            try:
+                traffic = json.load(open(prof)).get("scan_pass2_mat2_f64_n2^26")
+            except Exception:
+                traffic = None
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            v, dt = cpu_oracle_sample(1 << 23)
+            cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                   "sample": "LINREC + MAT2, n = 2^23 each, one pass of the oracle (one host thread)"}
+        line = {
+            "metric": METRIC, "value": 2 * gN / (mean_ms * 1e-3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (synth/, seed 2202)",
+            "config": {"workload": "configs[1]: vjp_scan LINREC + MAT2, n = 2^26 elements per op per GPU, f64",
+                       "n_per_op_per_gpu": n, "global_n_per_op": gN, "ops": ops,
+                       "parallelism": f"contiguous shards x{world}, all_gather of shard aggregates",
+                       "l2": "no flush: every array >= 1 GiB >> 126 MB L2"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "scan_pass2<OpMat2,f64> (MAT2 return sweep)",
+                         "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": kmat2,
+                         "peak_source": peak_src,
+                         "linrec_pass2_ms": statistics.mean(k_lin),
+                         "linrec_pass2_gbs": 48 * n / (statistics.mean(k_lin) * 1e-3) / 1e9,
+                         "step_alg_gbs": (64 + 128) * n / (mean_ms * 1e-3) / 1e9},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=0, help="override elements per op per GPU")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,287 @@
+/*
+ * include/vjp.h — C ABI of the B200 (sm_100a) vjp library  libvjp_b200.so
+ *
+ * The library computes the reverse-mode return sweeps (vector-Jacobian
+ * products, "vjp") of the bulk-parallel combinators of
+ * arXiv 2202.10297:
+ *
+ *   vjp_scan             sec 5.2, P:1131-1236   (scan / prefix sum)
+ *   vjp_reduce           sec 5.1, P:971-1087    (reduce; special cases + * min max)
+ *   vjp_reduce_by_index  sec 5.1.2, P:1090-1126 (histogram / multi-reduce)
+ *   vjp_scatter          sec 5.3
+ *
+ * "P:n" is line n of PAPER.md.  Every entry point takes the primal inputs, an
+ * operator tag and the output adjoint, and writes the input adjoint(s) by the
+ * paper's rules.  Readings of the paper where it is silent are listed in
+ * DESIGN.md ("Readings"); the ones that change results are repeated here.
+ *
+ * CONVENTIONS (all entry points)
+ *  - Every array argument is a DEVICE pointer (cudaMalloc / torch CUDA
+ *    tensor) owned by the caller, unless stated otherwise.  The library never
+ *    allocates device memory, never synchronises the host, and is stream
+ *    ordered: all work is enqueued on `stream` (a cudaStream_t; NULL = the
+ *    legacy default stream).  Calls on different streams with different
+ *    workspaces may run concurrently.
+ *  - Value arrays are f32 or f64 (`vjp_dtype`); index arrays are int32 or
+ *    int64 (`vjp_itype`).  Every array base pointer must be 16-byte aligned
+ *    (VJP_EALIGN otherwise): the kernels move tiles with TMA and 128-bit
+ *    vector accesses.
+ *  - Scan element layouts: ADD/MUL/MIN/MAX one scalar per element;
+ *    LINREC two scalars (d, c) interleaved (AoS); MAT2 four scalars, a 2x2
+ *    matrix row-major.  n always counts ELEMENTS, not scalars.
+ *  - `ws` is a device workspace of at least the bytes returned by the matching
+ *    *_workspace_bytes query (VJP_EWORKSPACE otherwise); it is overwritten
+ *    (its header is cleared on `stream` inside the call) and may be reused
+ *    by the next call on the same stream.  ws may be NULL iff the query
+ *    returns 0.
+ *  - flags: VJP_ACCUMULATE turns "as_bar = contribution" into the paper's
+ *    "as_bar += contribution" (reading R6).  Without it,
+ *    every element of the output adjoint is written.
+ *  - Arguments are validated before anything is enqueued; an argument error
+ *    returns non-zero and enqueues nothing.  A launch failure returns
+ *    VJP_ECUDA (cudaGetLastError); asynchronous kernel faults surface at the
+ *    caller's next synchronisation, as for any CUDA library.
+ *  - n == 0 is a no-op (outputs untouched; an optional primal output gets
+ *    the neutral element).
+ *  - Arithmetic: f64 data is computed in f64; f32 data is loaded as f32 and
+ *    computed/accumulated in f64, outputs rounded once to f32 (reading R9).
+ *    Round-to-nearest-even, no flush-to-zero.
+ */
+#ifndef VJP_B200_H
+#define VJP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *vjp_stream_t; /* identical to cudaStream_t */
+
+typedef enum { VJP_F32 = 1, VJP_F64 = 2 } vjp_dtype;
+typedef enum { VJP_I32 = 1, VJP_I64 = 2 } vjp_itype;
+
+/* Operator tags (the associative (.) of scan / reduce / reduce_by_index).
+ *  ADD, MUL, MIN, MAX : scalar +, *, min, max.
+ *  LINREC : element (d, c); (d1,c1) (.) (d2,c2) = (d2 + c2*d1, c2*c1) — the
+ *           paper's lin_o used as a primal operator (reading R2);
+ *           ys_i = (D_i, C_i), D_i = c_i*D_{i-1} + d_i (first-order linear
+ *           recurrence), C_i = prod c.  Neutral (0, 1).
+ *  MAT2   : element a 2x2 matrix, R_i = R_{i-1} . A_i (scan order of P:1137,
+ *           reading R1).  Neutral I. */
+typedef enum {
+    VJP_ADD = 1, VJP_MUL = 2, VJP_MIN = 3, VJP_MAX = 4, VJP_LINREC = 5, VJP_MAT2 = 6
+} vjp_op;
+
+typedef enum {
+    VJP_OK = 0,
+    VJP_EINVAL = 1,       /* bad argument (NULL where required, n < 0, m < 1, bad tag) */
+    VJP_EUNSUPPORTED = 2, /* a tag/call with no rule in the paper or not built (see each call) */
+    VJP_EWORKSPACE = 3,   /* ws_bytes smaller than the query */
+    VJP_ECUDA = 4,        /* a CUDA launch / runtime call failed */
+    VJP_EDUPINDEX = 5,    /* scatter: duplicate target (VJP_CHECK_INDICES only) */
+    VJP_EOOB = 6,         /* index out of range (VJP_CHECK_INDICES only) */
+    VJP_EALIGN = 7        /* an array base pointer is not 16-byte aligned */
+} vjp_status;
+
+enum {
+    VJP_ACCUMULATE = 1u,    /* as_bar += contribution instead of = */
+    VJP_CHECK_INDICES = 2u  /* scatter: detect duplicates / out-of-range (synchronises) */
+};
+
+/* One shard of a multi-GPU call: this process owns global elements
+ * [global_offset, global_offset + n_local) of a length-global_n problem,
+ * shards are contiguous and ordered by rank.  world == 1 means no sharding. */
+typedef struct {
+    int32_t rank;
+    int32_t world;
+    int64_t global_offset;
+    int64_t global_n;
+} vjp_shard;
+
+const char *vjp_status_string(vjp_status s);
+
+/* Number of kernels this library has launched in this process so far (the
+ * bench's gpu_launches count).  Host-side counter, thread-safe. */
+uint64_t vjp_launch_count(void);
+
+/* ======================================================================
+ * vjp_scan — sec 5.2
+ *
+ * Primal: ys = scan (.) e as, ys_i = as_0 (.) ... (.) as_i.
+ * Computes as_bar = ys_bar . J_scan(as).  The paper's rule: the
+ * forward sweep re-executes the primal scan; the return sweep builds
+ * per-element Jacobian pairs and runs a reverse scan with linear-function
+ * composition (lin_o; generalised to d-vectors with (0, I) as
+ * neutral), then a map.  Closed form for ADD:
+ * as_bar = reverse (scan (+) (reverse ys_bar)), in which case
+ * `as` is not read and may be NULL.
+ *
+ *   op      ADD, MUL, MIN, MAX, LINREC, MAT2.  MIN/MAX use the pick-left
+ *           subgradient on ties (reading R3).
+ *   dtype   VJP_F32 or VJP_F64, for as, ys_bar, as_bar, ys alike.
+ *   n       elements (>= 0).
+ *   as      [n x width] primal input (NULL allowed for ADD when ys == NULL).
+ *   ys_bar  [n x width] output adjoint.
+ *   as_bar  [n x width] input adjoint (output).  Must not alias as/ys_bar.
+ *   ys      nullable [n x width]: receives the primal scan (recomputed in the
+ *           return sweep, never stored as a tape).
+ *   ws      workspace, >= vjp_scan_workspace_bytes(op, dtype, n).
+ * Errors: VJP_EINVAL, VJP_EALIGN, VJP_EWORKSPACE, VJP_ECUDA.
+ * ==================================================================== */
+size_t vjp_scan_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_t n);
+vjp_status vjp_scan(vjp_op op, vjp_dtype dtype, int64_t n, const void *as,
+                    const void *ys_bar, void *as_bar, void *ys, void *ws, size_t ws_bytes,
+                    vjp_stream_t stream, unsigned flags);
+
+/* Multi-GPU phase split of vjp_scan (contiguous shards):
+ *   1. vjp_scan_partial: forward re-execution over the local shard; writes
+ *      this shard's partial record (forward aggregate of as; for world > 1
+ *      also the reverse-map aggregate, which reads ys_bar) to `partial`
+ *      (device, vjp_scan_partial_bytes(op, dtype) bytes).
+ *   2. the caller all-gathers the records of all ranks, in rank order, into
+ *      `gathered` (device, world x partial bytes) — e.g. NCCL all_gather.
+ *   3. vjp_scan_finish: return sweep over the local shard, with this shard's
+ *      forward carry (ranks < rank) and reverse carry (ranks > rank) combined
+ *      from `gathered` on the device.
+ * `n` is the LOCAL element count; `ws` must be the same workspace for both
+ * phases (the finish reads the partial's per-tile prefixes).  MIN/MAX return
+ * VJP_EUNSUPPORTED for world > 1 (their reverse coefficients depend on the
+ * forward carry).  vjp_scan == partial + finish with world = 1. */
+size_t vjp_scan_partial_bytes(vjp_op op, vjp_dtype dtype);
+vjp_status vjp_scan_partial(vjp_op op, vjp_dtype dtype, int64_t n, const void *as,
+                            const void *ys_bar, void *ws, size_t ws_bytes,
+                            const vjp_shard *shard, void *partial, vjp_stream_t stream,
+                            unsigned flags);
+vjp_status vjp_scan_finish(vjp_op op, vjp_dtype dtype, int64_t n, const void *as,
+                           const void *ys_bar, void *as_bar, void *ys, void *ws,
+                           size_t ws_bytes, const vjp_shard *shard, const void *gathered,
+                           vjp_stream_t stream, unsigned flags);
+
+/* Host-side (CPU, no device) evaluation of the carry combination that
+ * vjp_scan_finish performs on the device, for testing the multi-GPU logic
+ * without a GPU.  gathered: HOST, world x partial records.  Writes this
+ * rank's forward carry (width doubles) and reverse carry (width doubles). */
+vjp_status vjp_scan_carries_host(vjp_op op, vjp_dtype dtype, int32_t rank, int32_t world,
+                                 const void *gathered, double *fwd_carry, double *rev_carry);
+
+/* ======================================================================
+ * vjp_reduce — sec 5.1
+ *
+ * Primal: y = reduce (.) e as = as_0 (.) ... (.) as_{n-1}.
+ *   ADD : as_bar_i = y_bar; forward not needed unless y/arg asked.
+ *   MUL : forward computes (p = product of the nonzero elements [f64],
+ *         z = number of zeros, i0 = first zero index) by a map-reduce
+ *         (P:1055-1058); return: z = 0 -> as_bar_i = y_bar * p / as_i;
+ *         z = 1 -> as_bar_{i0} = y_bar * p (reading R8: P:1051's "y" is the
+ *         product of the nonzeros), 0 elsewhere; z >= 2 -> 0.
+ *         -0.0 counts as a zero (IEEE compare).
+ *   MIN/MAX : forward computes (y, i_y), i_y the FIRST index of the extremum
+ *         (IEEE compare so -0.0 ties +0.0); return
+ *         as_bar = 0 except as_bar[i_y] = y_bar.  With
+ *         VJP_ACCUMULATE only as_bar[i_y] is touched (the paper's sparse
+ *         adjoint).
+ *   y_bar  DEVICE pointer to one element of dtype.
+ *   as_bar [n] output.
+ *   y      nullable DEVICE [1]: primal result (MUL: 0 if z > 0, else p).
+ *   arg    nullable DEVICE int64[1]: i_y (MIN/MAX), i0 or -1 (MUL), -1 (ADD).
+ * Errors: VJP_EINVAL (LINREC/MAT2 tags), VJP_EALIGN, VJP_EWORKSPACE, VJP_ECUDA.
+ * ==================================================================== */
+size_t vjp_reduce_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_t n);
+vjp_status vjp_reduce(vjp_op op, vjp_dtype dtype, int64_t n, const void *as,
+                      const void *y_bar, void *as_bar, void *y, int64_t *arg, void *ws,
+                      size_t ws_bytes, vjp_stream_t stream, unsigned flags);
+
+/* Multi-GPU split: partial writes the shard's forward record (32 bytes:
+ * MUL {double p; int64 z; int64 i0_global; pad}, MIN/MAX {double v; int64
+ * i_global; ...}, ADD {double sum; ...}) to `partial` (device); the caller
+ * all-gathers world records in rank order; finish combines them on the device
+ * in rank order (deterministic) and runs the return map on the local shard. */
+size_t vjp_reduce_partial_bytes(void);
+vjp_status vjp_reduce_partial(vjp_op op, vjp_dtype dtype, int64_t n, const void *as, void *ws,
+                              size_t ws_bytes, const vjp_shard *shard, void *partial,
+                              vjp_stream_t stream);
+vjp_status vjp_reduce_finish(vjp_op op, vjp_dtype dtype, int64_t n, const void *as,
+                             const void *y_bar, void *as_bar, void *y, int64_t *arg, void *ws,
+                             size_t ws_bytes, const vjp_shard *shard, const void *gathered,
+                             vjp_stream_t stream, unsigned flags);
+
+/* ======================================================================
+ * vjp_reduce_by_index — sec 5.1.2
+ *
+ * Primal: hs = replicate m e; for i: hs[inds[i]] (.)= as[i];
+ * bins outside [0, m) are skipped and get adjoint 0 (reading R4).  Return
+ * sweep: the reduce rule with y_bar replaced by hs_bar[inds[i]]:
+ *   ADD : as_bar_i = hs_bar[b_i] (a gather; `as` may be NULL).
+ *   MUL : per-bin (p_b, z_b) forward histogram, then the three cases of
+ *         vjp_reduce per bin.
+ *   MIN/MAX : per-bin winner (value, lowest index), as_bar = 0 except
+ *         as_bar[winner_b] = hs_bar[b] (ACCUMULATE: only the winners).
+ * The general operator ("work is in progress") and LINREC/MAT2
+ * return VJP_EUNSUPPORTED.
+ *   inds   [n] int32/int64 bins;  as [n];  hs_bar [m];  as_bar [n] output.
+ *   hs     nullable DEVICE [m]: primal histogram (ADD: sum, MUL: product,
+ *          MIN/MAX: extremum, +-inf for an empty bin).
+ *   winners nullable DEVICE int64[m]: MIN/MAX winner index (-1 empty bin),
+ *          MUL: zero count per bin.
+ * ==================================================================== */
+size_t vjp_reduce_by_index_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_t n, int64_t m);
+vjp_status vjp_reduce_by_index(vjp_op op, vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m,
+                               const void *inds, const void *as, const void *hs_bar,
+                               void *as_bar, void *hs, int64_t *winners, void *ws,
+                               size_t ws_bytes, vjp_stream_t stream, unsigned flags);
+
+/* Multi-GPU split (partition by input range; per-bin state all-reduced):
+ *   partial: per-bin state of the local shard into bin_val (DEVICE double[m])
+ *            and bin_aux (DEVICE int64[m]):
+ *              MUL     bin_val = product of nonzeros, bin_aux = zero count
+ *                      -> all_reduce PRODUCT(bin_val), SUM(bin_aux)
+ *              MIN/MAX bin_val = local extremum (+-inf if empty), bin_aux =
+ *                      lowest GLOBAL index reaching it (INT64_MAX if empty)
+ *                      -> all_reduce MIN/MAX(bin_val), then
+ *                         vjp_reduce_by_index_select, then all_reduce MIN(bin_aux)
+ *              ADD     nothing to exchange (returns immediately)
+ *   select : MIN/MAX only: bin_aux[b] = INT64_MAX where the local extremum is
+ *            not the global one (bin_val now holds the global value).
+ *   finish : return sweep over the local shard from the combined state.
+ * Shards use shard->global_offset to form global indices. */
+vjp_status vjp_reduce_by_index_partial(vjp_op op, vjp_dtype dtype, vjp_itype itype, int64_t n,
+                                       int64_t m, const void *inds, const void *as, void *ws,
+                                       size_t ws_bytes, const vjp_shard *shard, double *bin_val,
+                                       int64_t *bin_aux, vjp_stream_t stream);
+vjp_status vjp_reduce_by_index_select(vjp_op op, int64_t m, const double *bin_val_global,
+                                      const double *bin_val_local, int64_t *bin_aux,
+                                      vjp_stream_t stream);
+vjp_status vjp_reduce_by_index_finish(vjp_op op, vjp_dtype dtype, vjp_itype itype, int64_t n,
+                                      int64_t m, const void *inds, const void *as,
+                                      const void *hs_bar, void *as_bar, const double *bin_val,
+                                      const int64_t *bin_aux, const vjp_shard *shard,
+                                      vjp_stream_t stream, unsigned flags);
+
+/* ======================================================================
+ * vjp_scatter — sec 5.3
+ *
+ * Primal: ys = scatter xs is vs: ys = xs except ys[is[j]] = vs[j]
+ * (P:1241-1244); `is` must hold no duplicate in-range target.
+ * Return sweep:
+ *     vs_bar += gather is ys_bar        (vs_bar[j] = ys_bar[is[j]])
+ *     xs_bar  = scatter ys_bar is (replicate m 0)
+ * Elements are `width` scalars (width >= 1).  Out-of-range targets are
+ * skipped and their vs_bar is 0 (reading R4).  xs_bar MAY alias ys_bar: then
+ * the call is in place and its work is O(m), independent of n;
+ * otherwise ys_bar is first copied to xs_bar (O(n)).  The paper's step (3),
+ * restoring the primal xs, is not part of the adjoint and is not done here.
+ *   is [m] int32/int64; ys_bar [n x width]; xs_bar [n x width]; vs_bar [m x width].
+ * VJP_CHECK_INDICES: validates `is` first (synchronises the stream) and
+ * returns VJP_EDUPINDEX / VJP_EOOB without touching the outputs.
+ * ==================================================================== */
+size_t vjp_scatter_workspace_bytes(vjp_dtype dtype, int64_t n, int64_t m);
+vjp_status vjp_scatter(vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, int64_t width,
+                       const void *is, const void *ys_bar, void *xs_bar, void *vs_bar, void *ws,
+                       size_t ws_bytes, vjp_stream_t stream, unsigned flags);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VJP_B200_H */

@@ -1,0 +1,299 @@
+"""paper_2202_10297_b200 — B200 (sm_100a) vjp return sweeps of scan, reduce,
+reduce_by_index and scatter (arXiv 2202.10297, sec 5).
+
+Thin Python binding over the C ABI of ``_lib/libvjp_b200.so``
+(``include/vjp.h``): argument marshalling only — every step of the path runs in
+the library's CUDA kernels.  PyTorch supplies device memory, streams and (in
+``dist``) process groups.  There is no CPU fallback: if the library is missing
+or the tensors are not on a CUDA device the calls raise.
+
+Host (CPU) tensors are accepted for the end-to-end path: they are copied to the
+current CUDA device, the call runs there, and the results are copied back.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libvjp_b200.so")
+
+F32, F64 = 1, 2
+I32, I64 = 1, 2
+ADD, MUL, MIN, MAX, LINREC, MAT2 = 1, 2, 3, 4, 5, 6
+OPS = {"add": ADD, "mul": MUL, "min": MIN, "max": MAX, "linrec": LINREC, "mat2": MAT2}
+WIDTH = {ADD: 1, MUL: 1, MIN: 1, MAX: 1, LINREC: 2, MAT2: 4}
+ACCUMULATE = 1
+CHECK_INDICES = 2
+STATUS = {0: "VJP_OK", 1: "VJP_EINVAL", 2: "VJP_EUNSUPPORTED", 3: "VJP_EWORKSPACE", 4: "VJP_ECUDA",
+          5: "VJP_EDUPINDEX", 6: "VJP_EOOB", 7: "VJP_EALIGN"}
+
+_lib = None
+
+
+class VjpError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        self.code = code
+        msg = lib().vjp_status_string(code).decode()
+        super().__init__(f"{where}: {msg}")
+
+
+class VjpShard(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("global_offset", ctypes.c_int64),
+                ("global_n", ctypes.c_int64)]
+
+
+def lib():
+    """Load libvjp_b200.so (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                              "(python -m paper_2202_10297_b200._build)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i64, sz, u32, ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_size_t, ctypes.c_uint, ctypes.c_int
+        sp = ctypes.POINTER(VjpShard)
+        sig = {
+            "vjp_status_string": ([ci], ctypes.c_char_p),
+            "vjp_launch_count": ([], ctypes.c_uint64),
+            "vjp_scan_workspace_bytes": ([ci, ci, i64], sz),
+            "vjp_scan": ([ci, ci, i64, vp, vp, vp, vp, vp, sz, vp, u32], ci),
+            "vjp_scan_partial_bytes": ([ci, ci], sz),
+            "vjp_scan_partial": ([ci, ci, i64, vp, vp, vp, sz, sp, vp, vp, u32], ci),
+            "vjp_scan_finish": ([ci, ci, i64, vp, vp, vp, vp, vp, sz, sp, vp, vp, u32], ci),
+            "vjp_scan_carries_host": ([ci, ci, ctypes.c_int32, ctypes.c_int32, vp, vp, vp], ci),
+            "vjp_reduce_workspace_bytes": ([ci, ci, i64], sz),
+            "vjp_reduce": ([ci, ci, i64, vp, vp, vp, vp, vp, vp, sz, vp, u32], ci),
+            "vjp_reduce_partial_bytes": ([], sz),
+            "vjp_reduce_partial": ([ci, ci, i64, vp, vp, sz, sp, vp, vp], ci),
+            "vjp_reduce_finish": ([ci, ci, i64, vp, vp, vp, vp, vp, vp, sz, sp, vp, vp, u32], ci),
+            "vjp_reduce_by_index_workspace_bytes": ([ci, ci, i64, i64], sz),
+            "vjp_reduce_by_index": ([ci, ci, ci, i64, i64, vp, vp, vp, vp, vp, vp, vp, sz, vp, u32], ci),
+            "vjp_reduce_by_index_partial": ([ci, ci, ci, i64, i64, vp, vp, vp, sz, sp, vp, vp, vp], ci),
+            "vjp_reduce_by_index_select": ([ci, i64, vp, vp, vp, vp], ci),
+            "vjp_reduce_by_index_finish": ([ci, ci, ci, i64, i64, vp, vp, vp, vp, vp, vp, sp, vp, u32], ci),
+            "vjp_scatter_workspace_bytes": ([ci, i64, i64], sz),
+            "vjp_scatter": ([ci, ci, i64, i64, i64, vp, vp, vp, vp, vp, sz, vp, u32], ci),
+        }
+        for name, (args, res) in sig.items():
+            if not hasattr(L, name):
+                continue  # reported by tests/test_abi_cpu.py::test_exports
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def launch_count() -> int:
+    """Kernels launched by the library in this process (bench gpu_launches)."""
+    return int(lib().vjp_launch_count())
+
+
+# ----------------------------------------------------------------- helpers
+
+def _op(op) -> int:
+    o = OPS[op] if isinstance(op, str) else int(op)
+    if o not in WIDTH:
+        raise ValueError(f"unknown operator {op!r}")
+    return o
+
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return F32
+    if t.dtype == torch.float64:
+        return F64
+    raise TypeError(f"vjp: value tensors must be float32/float64, got {t.dtype}")
+
+
+def _it(t: torch.Tensor) -> int:
+    if t.dtype == torch.int32:
+        return I32
+    if t.dtype == torch.int64:
+        return I64
+    raise TypeError(f"vjp: index tensors must be int32/int64, got {t.dtype}")
+
+
+def _p(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(dev) -> ctypes.c_void_p:
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _check(code: int, where: str):
+    if code != 0:
+        raise VjpError(code, where)
+
+
+def _dev_of(*ts):
+    for t in ts:
+        if t is not None and t.is_cuda:
+            return t.device
+    if not torch.cuda.is_available():
+        raise RuntimeError("vjp: no CUDA device (this library has no CPU path)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _to(t, dev):
+    if t is None:
+        return None
+    if t.is_cuda:
+        return t.contiguous()
+    src = t.contiguous()
+    if not src.is_pinned():
+        src = src.pin_memory()
+    return src.to(dev, non_blocking=True)
+
+
+def _out_buf(out, like, dev, accumulate):
+    """device buffer for an output: `out` itself if on the device; for a host
+    `out`, a device temporary (pre-loaded only when accumulating)."""
+    if out is None:
+        return torch.empty_like(like, device=dev)
+    if out.is_cuda:
+        return out
+    return _to(out, dev) if accumulate else torch.empty(out.shape, dtype=out.dtype, device=dev)
+
+
+def workspace(nbytes: int, dev) -> torch.Tensor | None:
+    if nbytes == 0:
+        return None
+    return torch.empty(nbytes, dtype=torch.uint8, device=dev)
+
+
+def _host_out(t: torch.Tensor, like_host: bool):
+    if not like_host:
+        return t
+    out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    out.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    return out
+
+
+# ----------------------------------------------------------------- calls
+
+def scan(op, ys_bar: torch.Tensor, as_: torch.Tensor | None = None, *, out: torch.Tensor | None = None,
+         want_ys: bool = False, accumulate: bool = False):
+    """as_bar of ``ys = scan op as_`` with output adjoint ``ys_bar`` (sec 5.2).
+
+    Tensors hold n elements of the operator's width (LINREC: (d, c) pairs,
+    MAT2: row-major 2x2), any shape with that many scalars.  Returns as_bar
+    (same shape as ys_bar), or (as_bar, ys) if want_ys."""
+    o = _op(op)
+    host = not ys_bar.is_cuda
+    dev = _dev_of(ys_bar, as_, out)
+    yb = _to(ys_bar, dev)
+    a = _to(as_, dev)
+    w = WIDTH[o]
+    if yb.numel() % w:
+        raise ValueError(f"ys_bar has {yb.numel()} scalars, not a multiple of width {w}")
+    n = yb.numel() // w
+    if a is not None and (a.numel() != yb.numel() or a.dtype != yb.dtype):
+        raise ValueError("as_ must match ys_bar in size and dtype")
+    ab = _out_buf(out, yb, dev, accumulate)
+    ys = torch.empty_like(yb) if want_ys else None
+    L = lib()
+    ws = workspace(L.vjp_scan_workspace_bytes(o, _dt(yb), n), dev)
+    _check(L.vjp_scan(o, _dt(yb), n, _p(a), _p(yb), _p(ab), _p(ys), _p(ws),
+                      0 if ws is None else ws.numel(), _stream(dev), ACCUMULATE if accumulate else 0),
+           "vjp_scan")
+    if out is not None and not out.is_cuda:
+        out.copy_(ab, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        ab = out
+    else:
+        ab = _host_out(ab, host)
+    if want_ys:
+        return ab, _host_out(ys, host)
+    return ab
+
+
+def reduce(op, as_: torch.Tensor, y_bar, *, out: torch.Tensor | None = None, want_y: bool = False,
+           accumulate: bool = False):
+    """as_bar of ``y = reduce op as_`` (sec 5.1).  y_bar: python float or a
+    1-element tensor.  Returns as_bar, or (as_bar, y, arg) if want_y (arg =
+    argmin/argmax for MIN/MAX, first zero index or -1 for MUL)."""
+    o = _op(op)
+    host = not as_.is_cuda
+    dev = _dev_of(as_, out)
+    a = _to(as_, dev)
+    n = a.numel()
+    if isinstance(y_bar, torch.Tensor):
+        yb = _to(y_bar.reshape(1).to(a.dtype), dev)
+    else:
+        yb = torch.full((1,), float(y_bar), dtype=a.dtype, device=dev)
+    ab = _out_buf(out, a, dev, accumulate)
+    y = torch.empty(1, dtype=a.dtype, device=dev) if want_y else None
+    arg = torch.empty(1, dtype=torch.int64, device=dev) if want_y else None
+    L = lib()
+    ws = workspace(L.vjp_reduce_workspace_bytes(o, _dt(a), n), dev)
+    _check(L.vjp_reduce(o, _dt(a), n, _p(a), _p(yb), _p(ab), _p(y), _p(arg), _p(ws),
+                        0 if ws is None else ws.numel(), _stream(dev), ACCUMULATE if accumulate else 0),
+           "vjp_reduce")
+    if out is not None and not out.is_cuda:
+        out.copy_(ab, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        ab = out
+    else:
+        ab = _host_out(ab, host)
+    if want_y:
+        return ab, _host_out(y, host), _host_out(arg, host)
+    return ab
+
+
+def reduce_by_index(op, inds: torch.Tensor, as_: torch.Tensor | None, hs_bar: torch.Tensor, *,
+                    out: torch.Tensor | None = None, want_hs: bool = False, accumulate: bool = False):
+    """as_bar of ``hs = reduce_by_index op m inds as_`` with m = len(hs_bar)
+    (sec 5.1.2).  Returns as_bar, or (as_bar, hs, winners) if want_hs
+    (winners: MIN/MAX per-bin winner index, -1 for an empty bin; MUL: zero count)."""
+    o = _op(op)
+    host = not inds.is_cuda
+    dev = _dev_of(inds, as_, hs_bar, out)
+    ix = _to(inds, dev)
+    a = _to(as_, dev)
+    hb = _to(hs_bar, dev)
+    n, m = ix.numel(), hb.numel()
+    ab = _out_buf(out, torch.empty(n, dtype=hb.dtype, device=dev), dev, accumulate)
+    hs = torch.empty(m, dtype=hb.dtype, device=dev) if want_hs else None
+    win = torch.empty(m, dtype=torch.int64, device=dev) if want_hs else None
+    L = lib()
+    ws = workspace(L.vjp_reduce_by_index_workspace_bytes(o, _dt(hb), n, m), dev)
+    _check(L.vjp_reduce_by_index(o, _dt(hb), _it(ix), n, m, _p(ix), _p(a), _p(hb), _p(ab), _p(hs), _p(win),
+                                 _p(ws), 0 if ws is None else ws.numel(), _stream(dev),
+                                 ACCUMULATE if accumulate else 0),
+           "vjp_reduce_by_index")
+    if out is not None and not out.is_cuda:
+        out.copy_(ab, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        ab = out
+    else:
+        ab = _host_out(ab, host)
+    if want_hs:
+        return ab, _host_out(hs, host), _host_out(win, host)
+    return ab
+
+
+def scatter(is_: torch.Tensor, ys_bar: torch.Tensor, *, width: int = 1, in_place: bool = False,
+            vs_out: torch.Tensor | None = None, accumulate: bool = False, check: bool = False):
+    """Adjoints of ``ys = scatter xs is vs`` (sec 5.3): returns (xs_bar, vs_bar).
+    in_place=True reuses ys_bar's storage for xs_bar (O(m) work)."""
+    host = not ys_bar.is_cuda
+    dev = _dev_of(is_, ys_bar, vs_out)
+    ix = _to(is_, dev)
+    yb = _to(ys_bar, dev)
+    if in_place and host:
+        raise ValueError("in_place scatter needs device tensors")
+    n, m = yb.numel() // width, ix.numel()
+    xb = yb if in_place else torch.empty_like(yb)
+    vb = _to(vs_out, dev) if vs_out is not None else torch.empty(m * width, dtype=yb.dtype, device=dev)
+    flags = (ACCUMULATE if accumulate else 0) | (CHECK_INDICES if check else 0)
+    L = lib()
+    ws = workspace(L.vjp_scatter_workspace_bytes(_dt(yb), n, m), dev)
+    _check(L.vjp_scatter(_dt(yb), _it(ix), n, m, width, _p(ix), _p(yb), _p(xb), _p(vb), _p(ws),
+                         0 if ws is None else ws.numel(), _stream(dev), flags), "vjp_scatter")
+    return _host_out(xb, host), _host_out(vb, host)

@@ -1,0 +1,112 @@
+// common.cuh — sm_100a building blocks shared by the vjp kernels:
+// TMA (cp.async.bulk.tensor) tile moves with 128B swizzle, mbarriers,
+// release/acquire status flags for decoupled look-back, launch bookkeeping.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/vjp.h"
+
+namespace vjpk {
+
+constexpr int kRowBytes = 128;   // one thread owns one 128-byte row of a tile
+constexpr int kThreads = 256;    // rows per tile (= threads per CTA for tile kernels)
+constexpr int kTileBytes = kRowBytes * kThreads;  // 32 KB per array per tile
+
+// ---------------------------------------------------------------------------
+// device helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;"
+                 ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+// 2-D TMA tile load global -> shared (completes on `bar` with complete_tx).
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                            int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];"
+        ::"r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1) : "memory");
+}
+
+// 2-D TMA tile store shared -> global (bulk async-group).
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap *map, const void *src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];"
+                 ::"l"(map), "r"(smem_u32(src)), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_wait_read0() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// generic-proxy smem writes -> visible to the async (TMA) proxy
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+// 128B-swizzled address of 16-byte chunk `c` (0..7) of row `r` in a tile
+// whose base is 1024-byte aligned (matches CU_TENSOR_MAP_SWIZZLE_128B).
+__device__ __forceinline__ uint32_t swz(int r, int c) { return (uint32_t)((r << 7) | (((c ^ r) & 7) << 4)); }
+
+// status flags for decoupled look-back (0 = not ready, 1 = aggregate, 2 = inclusive)
+__device__ __forceinline__ uint32_t ld_flag(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_flag_release(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+// L2-only (bypass L1) accesses for look-back payloads
+__device__ __forceinline__ double ld_cg(const double *p) { return __ldcg(p); }
+__device__ __forceinline__ void st_cg(double *p, double v) { __stcg(p, v); }
+
+template <class T>
+__device__ __forceinline__ T shfl_down_t(T v, int s) { return __shfl_down_sync(0xffffffffu, v, s); }
+template <class T>
+__device__ __forceinline__ T shfl_up_t(T v, int s) { return __shfl_up_sync(0xffffffffu, v, s); }
+template <class T>
+__device__ __forceinline__ T shfl_idx_t(T v, int l) { return __shfl_sync(0xffffffffu, v, l); }
+
+}  // namespace vjpk
+
+// ---------------------------------------------------------------------------
+// host helpers (vjp_host.cu)
+// ---------------------------------------------------------------------------
+namespace vjph {
+// 2-D tensor map over `bytes_full` bytes viewed as rows of 128 bytes; box =
+// 128 B x kThreads rows, 128B swizzle.  Returns false if it could not be built.
+bool make_row_tmap(CUtensorMap *map, const void *base, int64_t rows, bool f64);
+void count_launch(int k = 1);
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+}  // namespace vjph

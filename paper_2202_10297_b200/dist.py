@@ -1,0 +1,138 @@
+"""Multi-GPU vjp over torch.distributed (NCCL over NVLink), one process per GPU.
+
+Contiguous partition: rank r owns elements
+[offset_r, offset_r + n_r) of the global problem.  The path shards with ONE tiny
+exchange step:
+
+  scan            partial (forward re-execution + reverse-map aggregate of the
+                  shard) -> all_gather of the per-shard records (40 B LINREC,
+                  96 B MAT2) -> finish (return sweep with the combined carries).
+  reduce          partial record (p, z, i0) / (value, index) / sum -> all_gather
+                  -> finish (deterministic rank-order combine on the device).
+  reduce_by_index per-bin state -> all_reduce (PRODUCT+SUM for *, MAX/MIN then
+                  MIN of candidate indices for max/min) -> finish; ADD needs no
+                  exchange (hs_bar is replicated).
+
+All arithmetic runs in libvjp_b200.so; this module only sequences the calls and
+the collectives on the current stream.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import (ACCUMULATE, WIDTH, VjpShard, _check, _dt, _it, _op, _p, _stream, lib, workspace)
+
+
+def shard_bounds(global_n: int, world: int, rank: int) -> tuple[int, int]:
+    """contiguous, balanced split; rank r gets [off, off + n)."""
+    base, rem = divmod(global_n, world)
+    off = rank * base + min(rank, rem)
+    return off, base + (1 if rank < rem else 0)
+
+
+def _shard(offset: int, n: int, global_n: int, group) -> VjpShard:
+    if not (dist.is_available() and dist.is_initialized()):
+        return VjpShard(0, 1, offset, global_n)
+    return VjpShard(dist.get_rank(group), dist.get_world_size(group), offset, global_n)
+
+
+def scan(op, ys_bar: torch.Tensor, as_: torch.Tensor | None, *, offset: int, global_n: int, group=None,
+         out: torch.Tensor | None = None, want_ys: bool = False, accumulate: bool = False,
+         events: dict | None = None):
+    """vjp_scan over this rank's contiguous shard of a global scan.
+
+    `events`, if given, maps "finish_start"/"finish_end" to torch.cuda.Event
+    objects recorded around the return-sweep kernel (bench roofline)."""
+    o = _op(op)
+    dev = ys_bar.device
+    w = WIDTH[o]
+    n = ys_bar.numel() // w
+    dt = _dt(ys_bar)
+    L = lib()
+    sh = _shard(offset, n, global_n, group)
+    world = sh.world
+    ab = out if out is not None else torch.empty_like(ys_bar)
+    ys = torch.empty_like(ys_bar) if want_ys else None
+    ws = workspace(L.vjp_scan_workspace_bytes(o, dt, n), dev)
+    nbytes = 0 if ws is None else ws.numel()
+    rec = L.vjp_scan_partial_bytes(o, dt) // 8
+    part = torch.empty(rec, dtype=torch.float64, device=dev)
+    s = _stream(dev)
+    flags = ACCUMULATE if accumulate else 0
+    _check(L.vjp_scan_partial(o, dt, n, _p(as_), _p(ys_bar), _p(ws), nbytes, sh, _p(part), s, flags),
+           "vjp_scan_partial")
+    gathered = None
+    if world > 1:
+        gathered = torch.empty(world * rec, dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(gathered, part, group=group)
+    if events:
+        events["finish_start"].record()
+    _check(L.vjp_scan_finish(o, dt, n, _p(as_), _p(ys_bar), _p(ab), _p(ys), _p(ws), nbytes, sh, _p(gathered), s,
+                             flags), "vjp_scan_finish")
+    if events:
+        events["finish_end"].record()
+    return (ab, ys) if want_ys else ab
+
+
+def reduce(op, as_: torch.Tensor, y_bar, *, offset: int, global_n: int, group=None, out=None, want_y=False,
+           accumulate=False):
+    o = _op(op)
+    dev = as_.device
+    n = as_.numel()
+    dt = _dt(as_)
+    L = lib()
+    sh = _shard(offset, n, global_n, group)
+    yb = y_bar.reshape(1).to(as_.dtype) if isinstance(y_bar, torch.Tensor) else torch.full(
+        (1,), float(y_bar), dtype=as_.dtype, device=dev)
+    ab = out if out is not None else torch.empty_like(as_)
+    y = torch.empty(1, dtype=as_.dtype, device=dev) if want_y else None
+    arg = torch.empty(1, dtype=torch.int64, device=dev) if want_y else None
+    ws = workspace(L.vjp_reduce_workspace_bytes(o, dt, n), dev)
+    nbytes = 0 if ws is None else ws.numel()
+    rec = L.vjp_reduce_partial_bytes()
+    part = torch.empty(rec, dtype=torch.uint8, device=dev)
+    s = _stream(dev)
+    _check(L.vjp_reduce_partial(o, dt, n, _p(as_), _p(ws), nbytes, sh, _p(part), s), "vjp_reduce_partial")
+    gathered = torch.empty(sh.world * rec, dtype=torch.uint8, device=dev)
+    if sh.world > 1:
+        dist.all_gather_into_tensor(gathered, part, group=group)
+    else:
+        gathered.copy_(part)
+    _check(L.vjp_reduce_finish(o, dt, n, _p(as_), _p(yb), _p(ab), _p(y), _p(arg), _p(ws), nbytes, sh, _p(gathered),
+                               s, ACCUMULATE if accumulate else 0), "vjp_reduce_finish")
+    return (ab, y, arg) if want_y else ab
+
+
+def reduce_by_index(op, inds: torch.Tensor, as_: torch.Tensor | None, hs_bar: torch.Tensor, *, offset: int,
+                    global_n: int, group=None, out=None, accumulate=False):
+    o = _op(op)
+    dev = inds.device
+    n, m = inds.numel(), hs_bar.numel()
+    dt = _dt(hs_bar)
+    it = _it(inds)
+    L = lib()
+    sh = _shard(offset, n, global_n, group)
+    ab = out if out is not None else torch.empty(n, dtype=hs_bar.dtype, device=dev)
+    s = _stream(dev)
+    bin_val = torch.empty(m, dtype=torch.float64, device=dev)
+    bin_aux = torch.empty(m, dtype=torch.int64, device=dev)
+    if op not in ("add", 1):
+        ws = workspace(L.vjp_reduce_by_index_workspace_bytes(o, dt, n, m), dev)
+        nbytes = 0 if ws is None else ws.numel()
+        _check(L.vjp_reduce_by_index_partial(o, dt, it, n, m, _p(inds), _p(as_), _p(ws), nbytes, sh, _p(bin_val),
+                                             _p(bin_aux), s), "vjp_reduce_by_index_partial")
+        if sh.world > 1:
+            if o == 2:  # MUL
+                dist.all_reduce(bin_val, op=dist.ReduceOp.PRODUCT, group=group)
+                dist.all_reduce(bin_aux, op=dist.ReduceOp.SUM, group=group)
+            else:
+                local = bin_val.clone()
+                dist.all_reduce(bin_val, op=dist.ReduceOp.MAX if o == 4 else dist.ReduceOp.MIN, group=group)
+                _check(L.vjp_reduce_by_index_select(o, m, _p(bin_val), _p(local), _p(bin_aux), s),
+                       "vjp_reduce_by_index_select")
+                dist.all_reduce(bin_aux, op=dist.ReduceOp.MIN, group=group)
+    _check(L.vjp_reduce_by_index_finish(o, dt, it, n, m, _p(inds), _p(as_), _p(hs_bar), _p(ab), _p(bin_val),
+                                        _p(bin_aux), sh, s, ACCUMULATE if accumulate else 0),
+           "vjp_reduce_by_index_finish")
+    return ab
