@@ -86,8 +86,11 @@ typedef enum {
 } vjp_status;
 
 enum {
-    VJP_ACCUMULATE = 1u,    /* as_bar += contribution instead of = */
-    VJP_CHECK_INDICES = 2u  /* scatter: detect duplicates / out-of-range (synchronises) */
+    VJP_ACCUMULATE = 1u,     /* as_bar += contribution instead of = */
+    VJP_CHECK_INDICES = 2u,  /* scatter: detect duplicates / out-of-range (synchronises) */
+    VJP_SCAN_LOOKBACK = 1u << 16 /* tuning/testing: vjp_scan uses the single-sweep decoupled
+                                    look-back kernels instead of the chunked reduce-then-scan
+                                    kernels (MIN/MAX always use look-back) */
 };
 
 /* One shard of a multi-GPU call: this process owns global elements

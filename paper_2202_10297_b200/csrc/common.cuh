@@ -64,6 +64,12 @@ __device__ __forceinline__ void tma_store_wait_read0() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 // generic-proxy smem writes -> visible to the async (TMA) proxy
+__device__ __forceinline__ void tma_store_wait_read1() {
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -105,7 +111,8 @@ __device__ __forceinline__ T shfl_idx_t(T v, int l) { return __shfl_sync(0xfffff
 namespace vjph {
 // 2-D tensor map over `bytes_full` bytes viewed as rows of 128 bytes; box =
 // 128 B x kThreads rows, 128B swizzle.  Returns false if it could not be built.
-bool make_row_tmap(CUtensorMap *map, const void *base, int64_t rows, bool f64);
+bool make_row_tmap(CUtensorMap *map, const void *base, int64_t rows, bool f64, int box_rows = vjpk::kThreads);
+int sm_count();
 void count_launch(int k = 1);
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }

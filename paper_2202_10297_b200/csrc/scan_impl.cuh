@@ -5,7 +5,7 @@
 #include <mutex>
 #include <type_traits>
 
-#include "scan_kernels.cuh"
+#include "scan_chunked.cuh"
 
 namespace vjph {
 
@@ -36,9 +36,17 @@ struct ScanImpl {
     static constexpr int MD = Op::kMapD;
     static constexpr int R1MAX = W + MD;
 
+    // chunked path geometry (scan_chunked.cuh)
+    static constexpr int NTC = 128;  // rows (threads) per tile
+    static constexpr int SC = 3;     // TMA ring stages
+    static constexpr int kMaxChunks = 4096;
+    static constexpr int64_t TILE_C = (int64_t)G::EPR * NTC;
+
     struct Layout {
         int64_t ntiles;
-        size_t counters, flags1, flags2, memset_bytes, p1agg, p1inc, p2agg, p2inc, partial, total;
+        size_t counters, flags1, flags2, memset_bytes, p1agg, p1inc, p2agg, p2inc, partial;
+        int64_t ntiles_c;
+        size_t tileF, tileP, chunkRec, counter_c, total;
     };
     static Layout layout(int64_t n) {
         Layout L{};
@@ -53,6 +61,11 @@ struct ScanImpl {
         L.p2agg = off; off += align256((size_t)L.ntiles * MD * 8);
         L.p2inc = off; off += align256((size_t)L.ntiles * MD * 8);
         L.partial = off; off += align256((size_t)R1MAX * 8);
+        L.ntiles_c = n > 0 ? (n + TILE_C - 1) / TILE_C : 0;
+        L.tileF = off; off += align256((size_t)L.ntiles_c * W * 8);
+        L.tileP = off; off += align256((size_t)L.ntiles_c * W * 8);
+        L.chunkRec = off; off += align256((size_t)kMaxChunks * R1MAX * 8);
+        L.counter_c = off; off += 256;
         L.total = off;
         return L;
     }
@@ -127,11 +140,139 @@ struct ScanImpl {
         return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
     }
 
+    // ---------------- chunked reduce-then-scan path ----------------
+    static constexpr int SMALL = 4096;
+    static size_t smem_c(int nb) { return 1024 + (size_t)SC * nb * NTC * vjpk::kRowBytes + SMALL; }
+
+    static vjpk::ChunkParams cparams(const ScanCall &c, const Layout &L, int nchunks) {
+        vjpk::ChunkParams p{};
+        const int64_t bytes = c.n * (int64_t)G::ES;
+        p.n = c.n;
+        p.full_rows = bytes / vjpk::kRowBytes;
+        p.tail_bytes = (int32_t)(bytes % vjpk::kRowBytes);
+        p.ntiles = (int32_t)L.ntiles_c;
+        p.nchunks = nchunks;
+        p.as = c.as;
+        p.ys_bar = c.ys_bar;
+        p.as_bar = c.as_bar;
+        p.ys = c.ys;
+        unsigned char *ws = static_cast<unsigned char *>(c.ws);
+        p.tileF = reinterpret_cast<double *>(ws + L.tileF);
+        p.tileP = reinterpret_cast<double *>(ws + L.tileP);
+        p.chunkRec = reinterpret_cast<double *>(ws + L.chunkRec);
+        p.counter = reinterpret_cast<uint32_t *>(ws + L.counter_c);
+        p.partial = (c.world > 1) ? static_cast<double *>(c.partial) : nullptr;
+        p.gathered = static_cast<const double *>(c.gathered);
+        p.rank = c.rank;
+        p.world = c.world;
+        p.global_first = (c.global_offset == 0) ? 1 : 0;
+        return p;
+    }
+
+    template <class K>
+    static int occupancy(K kernel, size_t smem) {
+        set_smem(kernel, smem);
+        int nb = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, NTC, smem) != cudaSuccess || nb < 1) nb = 1;
+        return nb;
+    }
+
+    // one chunk per co-resident CTA of the heavier kernel (identical for both phases)
+    static int nchunks_for(const Layout &L, bool fwd, bool acc) {
+        constexpr int nbR = 2;
+        int occR = fwd ? occupancy(vjpk::scan_reduce<Op, T, NTC, SC, true, true>, smem_c(nbR))
+                       : occupancy(vjpk::scan_reduce<Op, T, NTC, SC, false, true>, smem_c(1));
+        int nbC = (fwd ? 1 : 0) + 1 + (acc ? 1 : 0);
+        int occC = fwd ? occupancy(vjpk::scan_apply<Op, T, NTC, SC, true, false, false>, smem_c(nbC))
+                       : occupancy(vjpk::scan_apply<Op, T, NTC, SC, false, false, false>, smem_c(nbC));
+        int per = occR < occC ? occR : occC;
+        int64_t g = (int64_t)sm_count() * per;
+        if (g > kMaxChunks) g = kMaxChunks;
+        if (g > L.ntiles_c) g = L.ntiles_c;
+        return (int)(g < 1 ? 1 : g);
+    }
+
+    static bool maps_c(const ScanCall &c, int64_t rows, CUtensorMap *m_as, CUtensorMap *m_yb, CUtensorMap *m_ab,
+                       CUtensorMap *m_ys) {
+        const bool f64 = sizeof(T) == 8;
+        bool ok = true;
+        ok &= make_row_tmap(m_as, c.as, c.as ? rows : 0, f64, NTC);
+        ok &= make_row_tmap(m_yb, c.ys_bar, rows, f64, NTC);
+        ok &= make_row_tmap(m_ab, c.as_bar, c.as_bar ? rows : 0, f64, NTC);
+        ok &= make_row_tmap(m_ys, c.ys, c.ys ? rows : 0, f64, NTC);
+        return ok;
+    }
+
+    template <bool FWD>
+    static vjp_status launch_reduce(const ScanCall &c, const vjpk::ChunkParams &p, const CUtensorMap &ma,
+                                    const CUtensorMap &my) {
+        constexpr int NB = (FWD ? 1 : 0) + 1;
+        auto k = vjpk::scan_reduce<Op, T, NTC, SC, FWD, true>;
+        size_t sm = smem_c(NB);
+        set_smem(k, sm);
+        k<<<(unsigned)p.nchunks, NTC, sm, c.stream>>>(ma, my, p);
+        count_launch();
+        return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+    }
+
+    template <bool FWD, bool ACC, bool YS>
+    static vjp_status launch_apply(const ScanCall &c, const vjpk::ChunkParams &p, const CUtensorMap &ma,
+                                   const CUtensorMap &my, const CUtensorMap &mab, const CUtensorMap &mys) {
+        constexpr int NB = (FWD ? 1 : 0) + 1 + (ACC ? 1 : 0);
+        auto k = vjpk::scan_apply<Op, T, NTC, SC, FWD, ACC, YS>;
+        size_t sm = smem_c(NB);
+        set_smem(k, sm);
+        k<<<(unsigned)p.nchunks, NTC, sm, c.stream>>>(ma, my, mab, mys, p);
+        count_launch();
+        return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+    }
+
+    static bool use_chunked(const ScanCall &c) {
+        return !Op::kRevNeedsRs && !(c.flags & VJP_SCAN_LOOKBACK);
+    }
+
+    static vjp_status partial_c(const ScanCall &c) {
+        Layout L = layout(c.n);
+        const bool fwd = need_fwd(c);
+        const int G = nchunks_for(L, fwd, (c.flags & VJP_ACCUMULATE) != 0);
+        vjpk::ChunkParams p = cparams(c, L, G);
+        if (c.world > 1 && cudaMemsetAsync(p.counter, 0, 4, c.stream) != cudaSuccess) return VJP_ECUDA;
+        CUtensorMap ma, my, mab, mys;
+        if (!maps_c(c, p.full_rows, &ma, &my, &mab, &mys)) return VJP_ECUDA;
+        if constexpr (std::is_same<Op, vjpk::OpAdd>::value) {
+            if (!fwd) return launch_reduce<false>(c, p, ma, my);
+        }
+        return launch_reduce<true>(c, p, ma, my);
+    }
+
+    static vjp_status finish_c(const ScanCall &c) {
+        Layout L = layout(c.n);
+        const bool fwd = need_fwd(c);
+        const bool acc = (c.flags & VJP_ACCUMULATE) != 0;
+        const int G = nchunks_for(L, fwd, acc);
+        vjpk::ChunkParams p = cparams(c, L, G);
+        CUtensorMap ma, my, mab, mys;
+        if (!maps_c(c, p.full_rows, &ma, &my, &mab, &mys)) return VJP_ECUDA;
+        const bool ys = c.ys != nullptr;
+        if constexpr (std::is_same<Op, vjpk::OpAdd>::value) {
+            if (!ys)
+                return acc ? launch_apply<false, true, false>(c, p, ma, my, mab, mys)
+                           : launch_apply<false, false, false>(c, p, ma, my, mab, mys);
+        }
+        if (acc) return ys ? launch_apply<true, true, true>(c, p, ma, my, mab, mys)
+                           : launch_apply<true, true, false>(c, p, ma, my, mab, mys);
+        return ys ? launch_apply<true, false, true>(c, p, ma, my, mab, mys)
+                  : launch_apply<true, false, false>(c, p, ma, my, mab, mys);
+    }
+
     static bool need_fwd(const ScanCall &c) {
         return !std::is_same<Op, vjpk::OpAdd>::value || c.ys != nullptr;
     }
 
     static vjp_status partial(const ScanCall &c) {
+        if constexpr (!Op::kRevNeedsRs) {
+            if (use_chunked(c)) return partial_c(c);
+        }
         Layout L = layout(c.n);
         vjpk::ScanParams p = params(c, L);
         if (cudaMemsetAsync(c.ws, 0, L.memset_bytes, c.stream) != cudaSuccess) return VJP_ECUDA;
@@ -150,6 +291,9 @@ struct ScanImpl {
     }
 
     static vjp_status finish(const ScanCall &c) {
+        if constexpr (!Op::kRevNeedsRs) {
+            if (use_chunked(c)) return finish_c(c);
+        }
         Layout L = layout(c.n);
         vjpk::ScanParams p = params(c, L);
         CUtensorMap ma, my, mab, mys;

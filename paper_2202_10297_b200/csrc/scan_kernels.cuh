@@ -155,7 +155,7 @@ __device__ __forceinline__ typename Op::Map shfl_idx_m(const typename Op::Map &m
 // ---- block-wide primitives (256 threads, 8 warps) --------------------------
 // exclusive forward scan of Val under fwd(); returns the thread's exclusive
 // prefix; `total` receives the block aggregate.  Uses scratch of 9 Vals.
-template <class Op>
+template <class Op, int NW = kThreads / 32>
 __device__ __forceinline__ typename Op::Val block_excl_fwd(typename Op::Val v, typename Op::Val *scr,
                                                            typename Op::Val &total) {
     using V = typename Op::Val;
@@ -169,28 +169,28 @@ __device__ __forceinline__ typename Op::Val block_excl_fwd(typename Op::Val v, t
     if (lane == 31) scr[warp] = inc;
     __syncthreads();
     if (warp == 0) {
-        V w = lane < 8 ? scr[lane] : Op::fwd_id();
+        V w = lane < NW ? scr[lane] : Op::fwd_id();
         V wi = w;
 #pragma unroll
-        for (int s = 1; s < 8; s <<= 1) {
+        for (int s = 1; s < NW; s <<= 1) {
             V o = shfl_up_v(wi, s);
             if (lane >= s) wi = Op::fwd(o, wi);
         }
         V we = shfl_up_v(wi, 1);
         if (lane == 0) we = Op::fwd_id();
-        if (lane < 8) scr[lane] = we;
-        if (lane == 7) scr[8] = wi;
+        if (lane < NW) scr[lane] = we;
+        if (lane == NW - 1) scr[NW] = wi;
     }
     __syncthreads();
     V ex = shfl_up_v(inc, 1);
     if (lane == 0) ex = Op::fwd_id();
     V r = Op::fwd(scr[warp], ex);
-    total = scr[8];
+    total = scr[NW];
     return r;
 }
 
 // ordered block reduce (fwd); result valid in all threads.
-template <class Op>
+template <class Op, int NW = kThreads / 32>
 __device__ __forceinline__ typename Op::Val block_reduce_fwd(typename Op::Val v, typename Op::Val *scr) {
     using V = typename Op::Val;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -203,14 +203,14 @@ __device__ __forceinline__ typename Op::Val block_reduce_fwd(typename Op::Val v,
     __syncthreads();
     V r = scr[0];
 #pragma unroll
-    for (int w = 1; w < 8; ++w) r = Op::fwd(r, scr[w]);
+    for (int w = 1; w < NW; ++w) r = Op::fwd(r, scr[w]);
     __syncthreads();
     return r;
 }
 
 // exclusive REVERSE scan of maps: thread t gets M_{t+1} o ... o M_255 (identity
 // for t = 255); `total` = M_0 o ... o M_255.  Scratch of 9 Maps.
-template <class Op>
+template <class Op, int NW = kThreads / 32>
 __device__ __forceinline__ typename Op::Map block_excl_rev(typename Op::Map m, typename Op::Map *scr,
                                                            typename Op::Map &total) {
     using M = typename Op::Map;
@@ -224,28 +224,28 @@ __device__ __forceinline__ typename Op::Map block_excl_rev(typename Op::Map m, t
     if (lane == 0) scr[warp] = inc;
     __syncthreads();
     if (warp == 0) {
-        M w = lane < 8 ? scr[lane] : Op::map_id();
-        M wi = w;  // W_lane o ... o W_7
+        M w = lane < NW ? scr[lane] : Op::map_id();
+        M wi = w;  // W_lane o ... o W_{NW-1}
 #pragma unroll
-        for (int s = 1; s < 8; s <<= 1) {
+        for (int s = 1; s < NW; s <<= 1) {
             M o = shfl_down_m<Op>(wi, s);
-            if (lane + s < 8) wi = Op::compose(wi, o);
+            if (lane + s < NW) wi = Op::compose(wi, o);
         }
         M we = shfl_down_m<Op>(wi, 1);
-        if (lane == 7) we = Op::map_id();
-        if (lane < 8) scr[lane] = we;
-        if (lane == 0) scr[8] = wi;
+        if (lane == NW - 1) we = Op::map_id();
+        if (lane < NW) scr[lane] = we;
+        if (lane == 0) scr[NW] = wi;
     }
     __syncthreads();
     M ex = shfl_down_m<Op>(inc, 1);
     if (lane == 31) ex = Op::map_id();
     M r = Op::compose(ex, scr[warp]);
-    total = scr[8];
+    total = scr[NW];
     return r;
 }
 
 // ordered block reduce of maps (M_0 o ... o M_255), valid in all threads.
-template <class Op>
+template <class Op, int NW = kThreads / 32>
 __device__ __forceinline__ typename Op::Map block_reduce_rev(typename Op::Map m, typename Op::Map *scr) {
     using M = typename Op::Map;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -258,7 +258,7 @@ __device__ __forceinline__ typename Op::Map block_reduce_rev(typename Op::Map m,
     __syncthreads();
     M r = scr[0];
 #pragma unroll
-    for (int w = 1; w < 8; ++w) r = Op::compose(r, scr[w]);
+    for (int w = 1; w < NW; ++w) r = Op::compose(r, scr[w]);
     __syncthreads();
     return r;
 }

@@ -28,7 +28,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 namespace vjph {
 void count_launch(int k) { g_launches.fetch_add((uint64_t)k, std::memory_order_relaxed); }
 
-bool make_row_tmap(CUtensorMap *map, const void *base, int64_t rows, bool f64) {
+bool make_row_tmap(CUtensorMap *map, const void *base, int64_t rows, bool f64, int box_rows) {
     std::memset(map, 0, sizeof(*map));
     if (rows <= 0) return true;  // never dereferenced by the kernels
     auto fn = encode_fn();
@@ -36,13 +36,19 @@ bool make_row_tmap(CUtensorMap *map, const void *base, int64_t rows, bool f64) {
     const cuuint64_t inner = f64 ? 16 : 32;
     cuuint64_t dims[2] = {inner, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)vjpk::kRowBytes};
-    cuuint32_t box[2] = {(cuuint32_t)inner, (cuuint32_t)vjpk::kThreads};
+    cuuint32_t box[2] = {(cuuint32_t)inner, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fn(map, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                     const_cast<void *>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
+}
+int sm_count() {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) return 148;
+    return n;
 }
 }  // namespace vjph
 

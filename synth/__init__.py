@@ -94,9 +94,13 @@ def linrec_inputs(n, *, dtype=torch.float64, offset=0, device="cpu"):
 
 
 def mat2_inputs(n, *, dtype=torch.float64, offset=0, device="cpu"):
-    """config 2 MAT2: 2x2 row-major entries ~ U(0, 0.5) (positive, spectral
-    radius < 1); seeds ~ U(0,1)^4."""
-    as_ = uniform(4 * n, 210, lo=0.0, hi=0.5, dtype=dtype, offset=4 * offset, device=device)
+    """config 2 MAT2: 2x2 row-stochastic (Markov transition) matrices
+    [[u, 1-u], [v, 1-v]], u, v ~ U(0,1): every prefix product stays
+    row-stochastic, so rs neither underflows nor overflows over 2^26 steps
+    (i.i.d. U(0, 1/2) entries would underflow to denormals after ~10^3 steps);
+    seeds ~ U(0,1)^4, all positive (no cancellation)."""
+    u = uniform(2 * n, 210, dtype=torch.float64, offset=2 * offset, device=device).reshape(n, 2)
+    as_ = torch.stack([u[:, 0], 1.0 - u[:, 0], u[:, 1], 1.0 - u[:, 1]], 1).reshape(-1).to(dtype)
     ybar = uniform(4 * n, 211, dtype=dtype, offset=4 * offset, device=device)
     return as_, ybar
 

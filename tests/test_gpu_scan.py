@@ -46,10 +46,10 @@ def make(op, n, dt, device="cpu"):
     raise ValueError(op)
 
 
-def run_both(op, n, dt, **kw):
+def run_both(op, n, dt, lookback=False):
     a, yb = make(op, n, dt)
-    ref = oracle.vjp_scan(op, yb.numpy(), None if a is None else a.numpy(), **kw)
-    got = vjp.scan(op, yb.to(DEV), None if a is None else a.to(DEV))
+    ref = oracle.vjp_scan(op, yb.numpy(), None if a is None else a.numpy())
+    got = vjp.scan(op, yb.to(DEV), None if a is None else a.to(DEV), lookback=lookback)
     torch.cuda.synchronize()
     return got.cpu().numpy(), ref
 
@@ -57,9 +57,18 @@ def run_both(op, n, dt, **kw):
 @pytest.mark.parametrize("dt", [np.float64, np.float32], ids=["f64", "f32"])
 @pytest.mark.parametrize("op", ["add", "mul", "min", "max", "linrec", "mat2"])
 def test_scan_parity_sizes(op, dt):
+    """default path (chunked reduce-then-scan; MIN/MAX: look-back)"""
     for n in SIZES:
         got, ref = run_both(op, n, dt)
         assert_close(got, ref, dt, what=f"{op} n={n}")
+
+
+@pytest.mark.parametrize("op", ["add", "mul", "linrec", "mat2"])
+def test_scan_parity_lookback_path(op):
+    """the single-sweep decoupled look-back kernels (VJP_SCAN_LOOKBACK)"""
+    for n in (1, 33, 1023, 4097, 100_003, 1_000_001):
+        got, ref = run_both(op, n, np.float64, lookback=True)
+        assert_close(got, ref, np.float64, what=f"lookback {op} n={n}")
 
 
 @pytest.mark.parametrize("dt", [np.float64, np.float32], ids=["f64", "f32"])
@@ -89,6 +98,10 @@ def test_scan_want_ys(op):
         a, yb = make(op, n, np.float64)
         if a is None:
             a = synth.uniform(n, 11, dtype=torch.float64)
+        if op == "linrec":  # keep prod(c) away from underflow so ys_C is comparable elementwise
+            a = a.reshape(n, 2).clone()
+            a[:, 1] = 1.0 + (synth.uniform(n, 13, dtype=torch.float64) - 0.5) / 64
+            a = a.reshape(-1)
         ref, ref_ys = oracle.vjp_scan(op, yb.numpy(), a.numpy(), want_ys=True)
         got, ys = vjp.scan(op, yb.to(DEV), a.to(DEV), want_ys=True)
         assert_close(got.cpu().numpy(), ref, np.float64, what=f"{op} as_bar n={n}")
