@@ -18,6 +18,12 @@
 //        primal scan in registers from the tile's prefix (tape-free), builds
 //        and reverse-scans the maps, applies the carry, writes as_bar (and ys).
 //
+// Inside a tile every thread owns one 128-byte row (a few elements) and folds
+// it serially; the per-row aggregates go to shared memory and ONE warp scans
+// each direction (warp 0 forward, warp 1 reverse: serial over NT/32 rows per
+// lane, then a 5-level shuffle scan), instead of every thread running a
+// shuffle tree of 2x2-map compositions.
+//
 // The return sweep therefore reads `as` and `ys_bar` twice (K_R, K_C) — the
 // same traffic the contiguous multi-GPU partition pays — in
 // exchange for pure streaming kernels.  For world > 1 the chunk records are
@@ -48,6 +54,62 @@ struct ChunkParams {
     int32_t rank, world;
     int32_t global_first;
 };
+
+// per-CTA shared scratch beside the TMA stages (sized on the host with sizeof).
+// Row aggregates are stored component-major with one pad slot per 16 entries
+// (spos) so that both the per-thread writes (entry = thread) and the scan
+// warp's reads (lane l reads entries l*K .. l*K+K-1) are bank-conflict free.
+template <int NT>
+struct RowArr {
+    static constexpr int kStride = NT + NT / 16;
+    __device__ static __forceinline__ int spos(int e) { return e + (e >> 4); }
+};
+template <class Op, int NT, int S>
+struct ReduceSmem {
+    uint64_t bar[S];
+    int last;
+    double rv[Op::W * RowArr<NT>::kStride];      // row forward aggregates
+    double rm[Op::kMapD * RowArr<NT>::kStride];  // row reverse maps
+    typename Op::Val vs[NT / 32 + 1];
+    typename Op::Map ms[NT / 32 + 1];
+};
+template <class Op, int NT, int S>
+struct ApplySmem {
+    uint64_t bar[S];
+    double rv[Op::W * RowArr<NT>::kStride];      // row forward aggregates -> rs entering each row
+    double rm[Op::kMapD * RowArr<NT>::kStride];  // row reverse maps; reused for H entering each row
+    typename Op::Val vs[NT / 32 + 1];
+    typename Op::Map ms[NT / 32 + 1];
+};
+
+template <int NT, int D>
+__device__ __forceinline__ void row_put(double *a, int e, const double *v) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) a[k * RowArr<NT>::kStride + RowArr<NT>::spos(e)] = v[k];
+}
+template <int NT, int D>
+__device__ __forceinline__ void row_get(const double *a, int e, double *v) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) v[k] = a[k * RowArr<NT>::kStride + RowArr<NT>::spos(e)];
+}
+template <class Op, int NT>
+__device__ __forceinline__ void put_v(double *a, int e, const typename Op::Val &v) { row_put<NT, Op::W>(a, e, v.x); }
+template <class Op, int NT>
+__device__ __forceinline__ typename Op::Val get_v(const double *a, int e) {
+    typename Op::Val v;
+    row_get<NT, Op::W>(a, e, v.x);
+    return v;
+}
+template <class Op, int NT>
+__device__ __forceinline__ void put_m(double *a, int e, const typename Op::Map &m) {
+    row_put<NT, Op::kMapD>(a, e, reinterpret_cast<const double *>(&m));
+}
+template <class Op, int NT>
+__device__ __forceinline__ typename Op::Map get_m(const double *a, int e) {
+    typename Op::Map m;
+    row_get<NT, Op::kMapD>(a, e, reinterpret_cast<double *>(&m));
+    return m;
+}
 
 __device__ __forceinline__ int64_t chunk_begin(const ChunkParams &p, int64_t c) {
     return c * (int64_t)p.ntiles / p.nchunks;
@@ -98,6 +160,141 @@ __device__ __forceinline__ void range_reduce(const double *recs, int64_t lo, int
     M = block_reduce_rev<Op, NW>(m, ms);
 }
 
+// ---- one thread's row: forward product and composed reverse map -----------
+template <class Op, class T, bool FWD>
+__device__ __forceinline__ typename Op::Val row_fwd(const unsigned char *sA, int t, int64_t e0, bool mask, int64_t n) {
+    using G = Geo<Op, T>;
+    typename Op::Val F = Op::fwd_id();
+    if constexpr (FWD) {
+#pragma unroll
+        for (int g = 0; g < G::NG; ++g) {
+            uint32_t w[G::GB / 4];
+            lds_group<G::GB>(sA, t, g, w);
+#pragma unroll
+            for (int e = 0; e < G::EG; ++e) {
+                typename Op::Val a = dec<T, Op::W>(w + e * (G::ES / 4));
+                if (!mask || e0 + g * G::EG + e < n) F = Op::fwd(F, a);
+            }
+        }
+    }
+    return F;
+}
+
+// M_e0 o ... o M_{e0+EPR-1}; rs-independent operators only (chunked path)
+template <class Op, class T, bool FWD>
+__device__ __forceinline__ typename Op::Map row_map(const unsigned char *sA, const unsigned char *sY, int t,
+                                                    int64_t e0, bool mask, int64_t n) {
+    using G = Geo<Op, T>;
+    typename Op::Map Tm = Op::map_id();
+#pragma unroll
+    for (int g = G::NG - 1; g >= 0; --g) {
+        uint32_t wa[G::GB / 4], wy[G::GB / 4];
+        if (FWD) lds_group<G::GB>(sA, t, g, wa);
+        lds_group<G::GB>(sY, t, g, wy);
+#pragma unroll
+        for (int e = G::EG - 1; e >= 0; --e) {
+            typename Op::Val a = FWD ? dec<T, Op::W>(wa + e * (G::ES / 4)) : Op::fwd_id();
+            typename Op::Val y = dec<T, Op::W>(wy + e * (G::ES / 4));
+            if (!mask || e0 + g * G::EG + e < n) Tm = Op::extend(Tm, Op::fwd_id(), a, y);
+        }
+    }
+    return Tm;
+}
+
+// ---- warp-level scans over the NT row aggregates in shared memory ----------
+// (executed by one full warp; lane l owns rows [l*K, l*K + K), K = NT/32)
+
+// reduce: returns v_0 (.) ... (.) v_{NT-1} in every lane
+template <class Op, int NT>
+__device__ __forceinline__ typename Op::Val warp_reduce_fwd_rows(const double *v) {
+    constexpr int K = NT / 32;
+    const int lane = threadIdx.x & 31;
+    typename Op::Val a = get_v<Op, NT>(v, lane * K);
+#pragma unroll
+    for (int j = 1; j < K; ++j) a = Op::fwd(a, get_v<Op, NT>(v, lane * K + j));
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+        typename Op::Val o = shfl_down_v(a, s);
+        if (lane + s < 32) a = Op::fwd(a, o);
+    }
+    return shfl_idx_v(a, 0);
+}
+template <class Op, int NT>
+__device__ __forceinline__ typename Op::Map warp_reduce_rev_rows(const double *m) {
+    constexpr int K = NT / 32;
+    const int lane = threadIdx.x & 31;
+    typename Op::Map a = get_m<Op, NT>(m, lane * K);
+#pragma unroll
+    for (int j = 1; j < K; ++j) a = Op::compose(a, get_m<Op, NT>(m, lane * K + j));
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+        typename Op::Map o = shfl_down_m<Op>(a, s);
+        if (lane + s < 32) a = Op::compose(a, o);
+    }
+    return shfl_idx_m<Op>(a, 0);
+}
+
+// exclusive forward scan, seeded with `pre`; overwrites v[r] with
+// pre (.) v_0 (.) ... (.) v_{r-1}
+template <class Op, int NT>
+__device__ __forceinline__ void warp_excl_fwd_rows(double *v, typename Op::Val pre) {
+    using V = typename Op::Val;
+    constexpr int K = NT / 32;
+    const int lane = threadIdx.x & 31;
+    V e[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) e[j] = get_v<Op, NT>(v, lane * K + j);
+    V loc = e[0];
+#pragma unroll
+    for (int j = 1; j < K; ++j) loc = Op::fwd(loc, e[j]);
+    V inc = loc;
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+        V o = shfl_up_v(inc, s);
+        if (lane >= s) inc = Op::fwd(o, inc);
+    }
+    V ex = shfl_up_v(inc, 1);
+    V r = lane == 0 ? pre : Op::fwd(pre, ex);
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        put_v<Op, NT>(v, lane * K + j, r);
+        r = Op::fwd(r, e[j]);
+    }
+}
+
+// reverse: given the maps m[r] of the rows and the carry X entering the tile
+// from the right, overwrites row r with (m_{r+1} o ... o m_{NT-1})(X) (the H
+// entering row r from the right, as a Val) and returns (m_0 o ... o m_{NT-1})(X) (the carry for
+// the next tile to the left) in every lane.
+template <class Op, int NT>
+__device__ __forceinline__ typename Op::Val warp_excl_rev_rows(double *m, typename Op::Val X) {
+    using V = typename Op::Val;
+    using M = typename Op::Map;
+    constexpr int K = NT / 32;
+    const int lane = threadIdx.x & 31;
+    M e[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) e[j] = get_m<Op, NT>(m, lane * K + j);
+    __syncwarp();  // the H values overwrite the maps in place
+    M loc = e[K - 1];
+#pragma unroll
+    for (int j = K - 2; j >= 0; --j) loc = Op::compose(e[j], loc);
+    M inc = loc;  // lanes l..31
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+        M o = shfl_down_m<Op>(inc, s);
+        if (lane + s < 32) inc = Op::compose(inc, o);
+    }
+    M ex = shfl_down_m<Op>(inc, 1);
+    V h = lane == 31 ? X : Op::apply(ex, X);
+#pragma unroll
+    for (int j = K - 1; j >= 0; --j) {
+        put_v<Op, NT>(m, lane * K + j, h);
+        h = Op::apply(e[j], h);
+    }
+    return shfl_idx_v(h, 0);
+}
+
 // =============================================================================
 // K_R: per-tile / per-chunk aggregates
 // =============================================================================
@@ -111,18 +308,13 @@ __global__ void __launch_bounds__(NT, 1) scan_reduce(const __grid_constant__ CUt
     constexpr int W = Op::W, NW = NT / 32, R = Op::W + Op::kMapD;
     constexpr int NB = (FWD ? 1 : 0) + (REV ? 1 : 0);
     constexpr int BUF = NT * kRowBytes, STG = NB * BUF;
+    static_assert(NW >= 2, "needs a forward and a reverse scan warp");
 
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    struct Small {
-        uint64_t bar[S];
-        int last;
-        V vs[NW + 1];
-        M ms[NW + 1];
-    };
-    Small &sm = *reinterpret_cast<Small *>(base + S * STG);
+    ReduceSmem<Op, NT, S> &sm = *reinterpret_cast<ReduceSmem<Op, NT, S> *>(base + S * STG);
 
-    const int t = threadIdx.x;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int64_t c = blockIdx.x;
     const int64_t t0 = chunk_begin(p, c), t1 = chunk_begin(p, c + 1), k = t1 - t0;
     const CUtensorMap *m0 = FWD ? &tm_as : &tm_yb;
@@ -133,7 +325,7 @@ __global__ void __launch_bounds__(NT, 1) scan_reduce(const __grid_constant__ CUt
     }
     __syncthreads();
 
-    V Fc = Op::fwd_id();
+    V Fc = Op::fwd_id();  // chunk aggregates, kept by warp 0 / warp 1
     M Mc = Op::map_id();
     for (int64_t i = 0; i < k; ++i) {
         const int64_t tile = t0 + i;
@@ -150,53 +342,32 @@ __global__ void __launch_bounds__(NT, 1) scan_reduce(const __grid_constant__ CUt
             __syncthreads();
         }
         const int64_t e0 = (tile * NT + t) * G::EPR;
-        V F = Op::fwd_id();
-        M Mt = Op::map_id();
-        if constexpr (FWD) {
-#pragma unroll
-            for (int g = 0; g < G::NG; ++g) {
-                uint32_t w[G::GB / 4];
-                lds_group<G::GB>(sA, t, g, w);
-#pragma unroll
-                for (int e = 0; e < G::EG; ++e) {
-                    V a = dec<T, W>(w + e * (G::ES / 4));
-                    if (!last || e0 + g * G::EG + e < p.n) F = Op::fwd(F, a);
-                }
-            }
-        }
-        if constexpr (REV) {
-#pragma unroll
-            for (int g = G::NG - 1; g >= 0; --g) {
-                uint32_t wa[G::GB / 4], wy[G::GB / 4];
-                if (FWD) lds_group<G::GB>(sA, t, g, wa);
-                lds_group<G::GB>(sY, t, g, wy);
-#pragma unroll
-                for (int e = G::EG - 1; e >= 0; --e) {
-                    V a = FWD ? dec<T, W>(wa + e * (G::ES / 4)) : Op::fwd_id();
-                    V y = dec<T, W>(wy + e * (G::ES / 4));
-                    if (!last || e0 + g * G::EG + e < p.n) Mt = Op::compose(Op::make_map(Op::fwd_id(), a, y), Mt);
-                }
-            }
-        }
-        V Ft = FWD ? block_reduce_fwd<Op, NW>(F, sm.vs) : F;
-        M Mtile = REV ? block_reduce_rev<Op, NW>(Mt, sm.ms) : Mt;
-        // the block reductions end in __syncthreads: stage s is free again
-        if (t == 0) {
-            if (FWD) {
+        V rowF = row_fwd<Op, T, FWD>(sA, t, e0, last, p.n);
+        M rowM = REV ? row_map<Op, T, FWD>(sA, sY, t, e0, last, p.n) : Op::map_id();
+        __syncthreads();  // every row read its data (stage s is free) and the scan warps are done with the scratch
+        if (t == 0 && i + S < k) issue_tile<NT, NB>(p, tile + S, &sm.bar[s], sA, m0, &tm_yb, &tm_yb);
+        if (FWD) put_v<Op, NT>(sm.rv, t, rowF);
+        if (REV) put_m<Op, NT>(sm.rm, t, rowM);
+        __syncthreads();
+        if (FWD && warp == 0) {
+            V Ft = warp_reduce_fwd_rows<Op, NT>(sm.rv);
+            if (lane == 0) {
 #pragma unroll
                 for (int q = 0; q < W; ++q) st_cg(p.tileF + tile * W + q, Ft.x[q]);
             }
-            if (i + S < k) issue_tile<NT, NB>(p, tile + S, &sm.bar[s], sA, m0, &tm_yb, &tm_yb);
+            Fc = Op::fwd(Fc, Ft);
         }
-        if (FWD) Fc = Op::fwd(Fc, Ft);
-        if (REV) Mc = Op::compose(Mc, Mtile);
+        if (REV && warp == 1) Mc = Op::compose(Mc, warp_reduce_rev_rows<Op, NT>(sm.rm));
     }
+    // chunk record [F | M]: F from warp 0, M from warp 1
     if (t == 0) {
-        double rec[R];
 #pragma unroll
-        for (int q = 0; q < W; ++q) rec[q] = Fc.x[q];
-        map_to<Op>(Mc, rec + W);
-        st_rec<R>(p.chunkRec + c * R, rec);
+        for (int q = 0; q < W; ++q) st_cg(p.chunkRec + c * R + q, Fc.x[q]);
+    }
+    if (t == 32) {
+        double rec[Op::kMapD];
+        map_to<Op>(Mc, rec);
+        st_rec<Op::kMapD>(p.chunkRec + c * R + W, rec);
     }
     if (p.partial) {
         // last-block pattern: the CTA that finishes last reduces all chunk
@@ -237,17 +408,13 @@ __global__ void __launch_bounds__(NT, 1) scan_apply(const __grid_constant__ CUte
     constexpr int W = Op::W, NW = NT / 32;
     constexpr int NB = (FWD ? 1 : 0) + 1 + (ACC ? 1 : 0);
     constexpr int BUF = NT * kRowBytes, STG = NB * BUF;
+    static_assert(NW >= 2, "needs a forward and a reverse scan warp");
 
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    struct Small {
-        uint64_t bar[S];
-        V vs[NW + 1];
-        M ms[NW + 1];
-    };
-    Small &sm = *reinterpret_cast<Small *>(base + S * STG);
+    ApplySmem<Op, NT, S> &sm = *reinterpret_cast<ApplySmem<Op, NT, S> *>(base + S * STG);
 
-    const int t = threadIdx.x;
+    const int t = threadIdx.x, warp = t >> 5;
     const int64_t c = blockIdx.x;
     const int64_t t0 = chunk_begin(p, c), t1 = chunk_begin(p, c + 1), k = t1 - t0;
     // stage buffer order: [A][Y][C]
@@ -266,7 +433,7 @@ __global__ void __launch_bounds__(NT, 1) scan_apply(const __grid_constant__ CUte
 #pragma unroll
     for (int q = 0; q < W; ++q) Hin.x[q] = 0.0;
     if (p.world > 1) shard_carries<Op>(p.gathered, p.rank, p.world, Fsh, Hin);
-    V X;  // H entering the current tile from the right
+    V X;  // H entering the current tile from the right (used by warp 1)
     {
         V Fpre, Fdummy;
         M Mdummy, Mpost;
@@ -304,7 +471,7 @@ __global__ void __launch_bounds__(NT, 1) scan_apply(const __grid_constant__ CUte
         const int64_t tile = t1 - 1 - i;
         const int s = (int)(i % S);
         V Ftile = Op::fwd_id();
-        if constexpr (FWD) {
+        if (FWD && warp == 0) {
 #pragma unroll
             for (int q = 0; q < W; ++q) Ftile.x[q] = ld_cg(p.tileP + tile * W + q);
         }
@@ -325,23 +492,19 @@ __global__ void __launch_bounds__(NT, 1) scan_apply(const __grid_constant__ CUte
         }
         const int64_t e0 = (tile * NT + t) * G::EPR;
 
-        // forward re-execution inside the tile (registers only)
+        // phase 1: row aggregates -> shared memory
+        if (FWD) put_v<Op, NT>(sm.rv, t, row_fwd<Op, T, FWD>(sA, t, e0, last, p.n));
+        put_m<Op, NT>(sm.rm, t, row_map<Op, T, FWD>(sA, sY, t, e0, last, p.n));
+        __syncthreads();
+        // block scans: warp 0 forward (rs entering each row), warp 1 reverse (H entering each row)
+        if (FWD && warp == 0) warp_excl_fwd_rows<Op, NT>(sm.rv, Ftile);
+        if (warp == 1) X = warp_excl_rev_rows<Op, NT>(sm.rm, X);
+        __syncthreads();
+
+        // phase 2: re-execute the primal scan over the row, then outputs right to left
         V rsp[G::EPR];
         if constexpr (FWD) {
-            V F = Op::fwd_id();
-#pragma unroll
-            for (int g = 0; g < G::NG; ++g) {
-                uint32_t w[G::GB / 4];
-                lds_group<G::GB>(sA, t, g, w);
-#pragma unroll
-                for (int e = 0; e < G::EG; ++e) {
-                    V a = dec<T, W>(w + e * (G::ES / 4));
-                    if (!last || e0 + g * G::EG + e < p.n) F = Op::fwd(F, a);
-                }
-            }
-            V tot;
-            V ex = block_excl_fwd<Op, NW>(F, sm.vs, tot);
-            V r = Op::fwd(Ftile, ex);
+            V r = get_v<Op, NT>(sm.rv, t);
 #pragma unroll
             for (int g = 0; g < G::NG; ++g) {
                 uint32_t w[G::GB / 4];
@@ -357,27 +520,7 @@ __global__ void __launch_bounds__(NT, 1) scan_apply(const __grid_constant__ CUte
 #pragma unroll
             for (int q = 0; q < G::EPR; ++q) rsp[q] = Op::fwd_id();
         }
-
-        // thread map and its block-wide reverse exclusive scan
-        M Tm = Op::map_id();
-#pragma unroll
-        for (int g = G::NG - 1; g >= 0; --g) {
-            uint32_t wa[G::GB / 4], wy[G::GB / 4];
-            if (FWD) lds_group<G::GB>(sA, t, g, wa);
-            lds_group<G::GB>(sY, t, g, wy);
-#pragma unroll
-            for (int e = G::EG - 1; e >= 0; --e) {
-                V a = FWD ? dec<T, W>(wa + e * (G::ES / 4)) : Op::fwd_id();
-                V y = dec<T, W>(wy + e * (G::ES / 4));
-                if (!last || e0 + g * G::EG + e < p.n) Tm = Op::compose(Op::make_map(rsp[g * G::EG + e], a, y), Tm);
-            }
-        }
-        M Agg;
-        M Nt = block_excl_rev<Op, NW>(Tm, sm.ms, Agg);
-        V Xr = Op::apply(Nt, X);   // H entering this thread's row from the right
-        X = Op::apply(Agg, X);     // carry for the next tile (to the left)
-
-        // outputs, right to left
+        V Xr = get_v<Op, NT>(sm.rm, t);
 #pragma unroll
         for (int g = G::NG - 1; g >= 0; --g) {
             uint32_t wa[G::GB / 4], wy[G::GB / 4], wc[G::GB / 4], wo[G::GB / 4], wz[G::GB / 4];
@@ -389,7 +532,6 @@ __global__ void __launch_bounds__(NT, 1) scan_apply(const __grid_constant__ CUte
                 const int q = g * G::EG + e;
                 V a = FWD ? dec<T, W>(wa + e * (G::ES / 4)) : Op::fwd_id();
                 V y = dec<T, W>(wy + e * (G::ES / 4));
-                const bool valid = !last || e0 + q < p.n;
                 V gv;
 #pragma unroll
                 for (int z = 0; z < W; ++z) gv.x[z] = y.x[z] + Xr.x[z];  // rbar_i = ybar_i + H_{i+1}
@@ -402,7 +544,7 @@ __global__ void __launch_bounds__(NT, 1) scan_apply(const __grid_constant__ CUte
                 }
                 enc<T, W>(o, wo + e * (G::ES / 4));
                 if (YS) enc<T, W>(Op::fwd(rsp[q], a), wz + e * (G::ES / 4));
-                if (valid) Xr = Op::apply(Op::make_map(rsp[q], a, y), Xr);
+                if (!last || e0 + q < p.n) Xr = Op::pass_left(rsp[q], a, gv);  // H_i = J_L^T rbar_i
             }
             sts_group<G::GB>(sY, t, g, wo);
             if (YS) sts_group<G::GB>(sA, t, g, wz);

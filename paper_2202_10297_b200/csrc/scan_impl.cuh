@@ -141,8 +141,12 @@ struct ScanImpl {
     }
 
     // ---------------- chunked reduce-then-scan path ----------------
-    static constexpr int SMALL = 4096;
-    static size_t smem_c(int nb) { return 1024 + (size_t)SC * nb * NTC * vjpk::kRowBytes + SMALL; }
+    static size_t smem_r(int nb) {
+        return 1024 + (size_t)SC * nb * NTC * vjpk::kRowBytes + sizeof(vjpk::ReduceSmem<Op, NTC, SC>);
+    }
+    static size_t smem_a(int nb) {
+        return 1024 + (size_t)SC * nb * NTC * vjpk::kRowBytes + sizeof(vjpk::ApplySmem<Op, NTC, SC>);
+    }
 
     static vjpk::ChunkParams cparams(const ScanCall &c, const Layout &L, int nchunks) {
         vjpk::ChunkParams p{};
@@ -180,11 +184,11 @@ struct ScanImpl {
     // one chunk per co-resident CTA of the heavier kernel (identical for both phases)
     static int nchunks_for(const Layout &L, bool fwd, bool acc) {
         constexpr int nbR = 2;
-        int occR = fwd ? occupancy(vjpk::scan_reduce<Op, T, NTC, SC, true, true>, smem_c(nbR))
-                       : occupancy(vjpk::scan_reduce<Op, T, NTC, SC, false, true>, smem_c(1));
+        int occR = fwd ? occupancy(vjpk::scan_reduce<Op, T, NTC, SC, true, true>, smem_r(nbR))
+                       : occupancy(vjpk::scan_reduce<Op, T, NTC, SC, false, true>, smem_r(1));
         int nbC = (fwd ? 1 : 0) + 1 + (acc ? 1 : 0);
-        int occC = fwd ? occupancy(vjpk::scan_apply<Op, T, NTC, SC, true, false, false>, smem_c(nbC))
-                       : occupancy(vjpk::scan_apply<Op, T, NTC, SC, false, false, false>, smem_c(nbC));
+        int occC = fwd ? occupancy(vjpk::scan_apply<Op, T, NTC, SC, true, false, false>, smem_a(nbC))
+                       : occupancy(vjpk::scan_apply<Op, T, NTC, SC, false, false, false>, smem_a(nbC));
         int per = occR < occC ? occR : occC;
         int64_t g = (int64_t)sm_count() * per;
         if (g > kMaxChunks) g = kMaxChunks;
@@ -208,7 +212,7 @@ struct ScanImpl {
                                     const CUtensorMap &my) {
         constexpr int NB = (FWD ? 1 : 0) + 1;
         auto k = vjpk::scan_reduce<Op, T, NTC, SC, FWD, true>;
-        size_t sm = smem_c(NB);
+        size_t sm = smem_r(NB);
         set_smem(k, sm);
         k<<<(unsigned)p.nchunks, NTC, sm, c.stream>>>(ma, my, p);
         count_launch();
@@ -220,7 +224,7 @@ struct ScanImpl {
                                    const CUtensorMap &my, const CUtensorMap &mab, const CUtensorMap &mys) {
         constexpr int NB = (FWD ? 1 : 0) + 1 + (ACC ? 1 : 0);
         auto k = vjpk::scan_apply<Op, T, NTC, SC, FWD, ACC, YS>;
-        size_t sm = smem_c(NB);
+        size_t sm = smem_a(NB);
         set_smem(k, sm);
         k<<<(unsigned)p.nchunks, NTC, sm, c.stream>>>(ma, my, mab, mys, p);
         count_launch();

@@ -22,6 +22,7 @@
 //   Map  (affine map on W-vector adjoints)      map_id(), compose(outer, inner),
 //        apply(M, X), constant(V) (C = 0: X -> V)
 //   make_map(rs_prev, a, ybar) = M_i ;  out(rs_prev, a, g) = J_R^T g
+//   pass_left(rs_prev, a, g) = J_L^T g ;  extend(T, rs_prev, a, ybar) = M_i o T
 #pragma once
 #include <math.h>
 
@@ -51,6 +52,9 @@ struct OpAdd {
     HD static Map constant(const Val &v) { return {v.x[0]}; }
     HD static Map make_map(const Val &, const Val &, const Val &yb) { return {yb.x[0]}; }
     HD static Val out(const Val &, const Val &, const Val &g) { return g; }
+    // pass_left = J_L^T g (the contribution to the carry); extend(T) = make_map o T
+    HD static Val pass_left(const Val &, const Val &, const Val &g) { return g; }
+    HD static Map extend(const Map &T, const Val &, const Val &, const Val &yb) { return {yb.x[0] + T.D}; }
 };
 
 // ------------------------------------------------------------------ MUL
@@ -70,6 +74,10 @@ struct OpMul {
     HD static Map constant(const Val &v) { return {v.x[0], 0.0}; }
     HD static Map make_map(const Val &, const Val &a, const Val &yb) { return {a.x[0] * yb.x[0], a.x[0]}; }
     HD static Val out(const Val &rp, const Val &, const Val &g) { return {{rp.x[0] * g.x[0]}}; }
+    HD static Val pass_left(const Val &, const Val &a, const Val &g) { return {{a.x[0] * g.x[0]}}; }
+    HD static Map extend(const Map &T, const Val &, const Val &a, const Val &yb) {
+        return {a.x[0] * (yb.x[0] + T.D), a.x[0] * T.C};
+    }
 };
 
 // ------------------------------------------------------------ MIN / MAX
@@ -95,6 +103,13 @@ struct OpExt {
     }
     HD static Val out(const Val &rp, const Val &a, const Val &g) {
         return {{left(rp.x[0], a.x[0]) ? 0.0 : g.x[0]}};
+    }
+    HD static Val pass_left(const Val &rp, const Val &a, const Val &g) {
+        return {{left(rp.x[0], a.x[0]) ? g.x[0] : 0.0}};
+    }
+    HD static Map extend(const Map &T, const Val &rp, const Val &a, const Val &yb) {
+        double jl = left(rp.x[0], a.x[0]) ? 1.0 : 0.0;
+        return {jl * (yb.x[0] + T.D), jl * T.C};
     }
 };
 using OpMin = OpExt<false>;
@@ -124,6 +139,11 @@ struct OpLinrec {
     }
     HD static Val out(const Val &rp, const Val &, const Val &g) {
         return {{g.x[0], g.x[0] * rp.x[0] + g.x[1] * rp.x[1]}};
+    }
+    HD static Val pass_left(const Val &, const Val &a, const Val &g) { return {{a.x[1] * g.x[0], a.x[1] * g.x[1]}}; }
+    HD static Map extend(const Map &T, const Val &, const Val &a, const Val &yb) {
+        double c = a.x[1];
+        return {c * (yb.x[0] + T.D0), c * (yb.x[1] + T.D1), c * T.C};
     }
 };
 
@@ -166,6 +186,18 @@ struct OpMat2 {
     HD static Val out(const Val &rp, const Val &, const Val &g) {
         Val Rt{{rp.x[0], rp.x[2], rp.x[1], rp.x[3]}};
         return mm(Rt, g);
+    }
+    HD static Val pass_left(const Val &, const Val &a, const Val &g) {  // g A^T
+        Val At{{a.x[0], a.x[2], a.x[1], a.x[3]}};
+        return mm(g, At);
+    }
+    HD static Map extend(const Map &T, const Val &, const Val &a, const Val &yb) {
+        // (X -> (yb + D + X C) A^T): D' = (yb + D) A^T, C' = C A^T
+        Val At{{a.x[0], a.x[2], a.x[1], a.x[3]}};
+        Val s{{yb.x[0] + T.D[0], yb.x[1] + T.D[1], yb.x[2] + T.D[2], yb.x[3] + T.D[3]}};
+        Val C{{T.C[0], T.C[1], T.C[2], T.C[3]}};
+        Val D2 = mm(s, At), C2 = mm(C, At);
+        return {{D2.x[0], D2.x[1], D2.x[2], D2.x[3]}, {C2.x[0], C2.x[1], C2.x[2], C2.x[3]}};
     }
 };
 
