@@ -259,8 +259,8 @@ vjp_status vjp_reduce_by_index_select(vjp_op op, int64_t m, const double *bin_va
 vjp_status vjp_reduce_by_index_finish(vjp_op op, vjp_dtype dtype, vjp_itype itype, int64_t n,
                                       int64_t m, const void *inds, const void *as,
                                       const void *hs_bar, void *as_bar, const double *bin_val,
-                                      const int64_t *bin_aux, const vjp_shard *shard,
-                                      vjp_stream_t stream, unsigned flags);
+                                      const int64_t *bin_aux, void *ws, size_t ws_bytes,
+                                      const vjp_shard *shard, vjp_stream_t stream, unsigned flags);
 
 /* ======================================================================
  * vjp_scatter — sec 5.3
@@ -277,7 +277,10 @@ vjp_status vjp_reduce_by_index_finish(vjp_op op, vjp_dtype dtype, vjp_itype ityp
  * restoring the primal xs, is not part of the adjoint and is not done here.
  *   is [m] int32/int64; ys_bar [n x width]; xs_bar [n x width]; vs_bar [m x width].
  * VJP_CHECK_INDICES: validates `is` first (synchronises the stream) and
- * returns VJP_EDUPINDEX / VJP_EOOB without touching the outputs.
+ * returns VJP_EDUPINDEX / VJP_EOOB without touching the outputs; it needs a
+ * workspace of vjp_scatter_workspace_bytes (a bitmap of n bits); without it
+ * ws may be NULL.  VJP_ACCUMULATE applies to vs_bar (the paper's +=); xs_bar
+ * is always the assignment of P:1275.
  * ==================================================================== */
 size_t vjp_scatter_workspace_bytes(vjp_dtype dtype, int64_t n, int64_t m);
 vjp_status vjp_scatter(vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, int64_t width,

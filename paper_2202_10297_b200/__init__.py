@@ -74,7 +74,7 @@ def lib():
             "vjp_reduce_by_index": ([ci, ci, ci, i64, i64, vp, vp, vp, vp, vp, vp, vp, sz, vp, u32], ci),
             "vjp_reduce_by_index_partial": ([ci, ci, ci, i64, i64, vp, vp, vp, sz, sp, vp, vp, vp], ci),
             "vjp_reduce_by_index_select": ([ci, i64, vp, vp, vp, vp], ci),
-            "vjp_reduce_by_index_finish": ([ci, ci, ci, i64, i64, vp, vp, vp, vp, vp, vp, sp, vp, u32], ci),
+            "vjp_reduce_by_index_finish": ([ci, ci, ci, i64, i64, vp, vp, vp, vp, vp, vp, vp, sz, sp, vp, u32], ci),
             "vjp_scatter_workspace_bytes": ([ci, i64, i64], sz),
             "vjp_scatter": ([ci, ci, i64, i64, i64, vp, vp, vp, vp, vp, sz, vp, u32], ci),
         }
@@ -261,6 +261,8 @@ def reduce_by_index(op, inds: torch.Tensor, as_: torch.Tensor | None, hs_bar: to
     a = _to(as_, dev)
     hb = _to(hs_bar, dev)
     n, m = ix.numel(), hb.numel()
+    if a is not None and (a.dtype != hb.dtype or a.numel() != n):
+        raise ValueError("as_ must have len(inds) elements of hs_bar's dtype")
     ab = _out_buf(out, torch.empty(n, dtype=hb.dtype, device=dev), dev, accumulate)
     hs = torch.empty(m, dtype=hb.dtype, device=dev) if want_hs else None
     win = torch.empty(m, dtype=torch.int64, device=dev) if want_hs else None
@@ -296,7 +298,7 @@ def scatter(is_: torch.Tensor, ys_bar: torch.Tensor, *, width: int = 1, in_place
     vb = _to(vs_out, dev) if vs_out is not None else torch.empty(m * width, dtype=yb.dtype, device=dev)
     flags = (ACCUMULATE if accumulate else 0) | (CHECK_INDICES if check else 0)
     L = lib()
-    ws = workspace(L.vjp_scatter_workspace_bytes(_dt(yb), n, m), dev)
+    ws = workspace(L.vjp_scatter_workspace_bytes(_dt(yb), n, m), dev) if check else None
     _check(L.vjp_scatter(_dt(yb), _it(ix), n, m, width, _p(ix), _p(yb), _p(xb), _p(vb), _p(ws),
                          0 if ws is None else ws.numel(), _stream(dev), flags), "vjp_scatter")
     return _host_out(xb, host), _host_out(vb, host)

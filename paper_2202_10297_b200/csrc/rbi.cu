@@ -1,0 +1,638 @@
+// rbi.cu — vjp_reduce_by_index (sec 5.1.2) for sm_100a.
+//
+// Forward sweep = the histogram with the operator extended as for reduce
+// (P:1120-1124); return sweep = the reduce rule with ybar replaced by
+// hs_bar[inds[i]].  Bins outside [0, m) are skipped (reading R4).
+//
+//   ADD      return sweep only: as_bar_i = hs_bar[b_i] — a streaming gather
+//            (hs_bar is L2 resident: 8 KB at m = 10^3, 8 MB at m = 10^6).
+//   MUL      forward: per-bin (p_b = product of the nonzeros, z_b = #zeros).
+//            small m: WARP-PRIVATE shared-memory histograms, conflicts inside
+//            a warp resolved with match.any (one lane per distinct bin per
+//            round), so no atomics on the hot loop; merged into global state
+//            once per CTA.  large m: global CAS-multiply + atomicAdd.
+//            return: per-bin q_b = hs_bar_b * p_b packed with z_b (one 16-byte
+//            gather per element), then the three cases of P:1043-1053.
+//   MIN/MAX  forward: per-bin winner = (extremum, LOWEST index) kept as a
+//            128-bit key {orderable value bits, ~index} (max wins) updated by
+//            atom.cas.b128 behind a monotone filter (skip when the stored
+//            value key is already larger — keys only grow), in shared memory
+//            for small m and in global memory for large m.  The dense return
+//            zero-fills as_bar inside the forward kernel (write stream) and
+//            then scatters hs_bar[b] to the m winners.
+#include "common.cuh"
+
+namespace vjpk {
+
+constexpr int kBThreads = 256;
+
+template <class I>
+struct IdxVec;
+template <>
+struct IdxVec<int32_t> {
+    static constexpr int N = 4;
+    using V = int4;
+    __device__ static __forceinline__ void get(const V &v, int64_t *o) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
+};
+template <>
+struct IdxVec<int64_t> {
+    static constexpr int N = 2;
+    using V = longlong2;
+    __device__ static __forceinline__ void get(const V &v, int64_t *o) { o[0] = v.x; o[1] = v.y; }
+};
+
+// ------------------------------------------------------------ key helpers
+// orderable 64-bit key of a double (total order = IEEE order on non-NaN,
+// -0.0 canonicalised to +0.0 so that the two tie, reading A9/R-tie)
+__device__ __forceinline__ uint64_t ord_key(double x, bool is_min) {
+    if (x == 0.0) x = 0.0;
+    uint64_t u = (uint64_t)__double_as_longlong(x);
+    u = (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+    return is_min ? ~u : u;  // min-reduction: larger key = smaller value
+}
+__device__ __forceinline__ double key_val(uint64_t k, bool is_min) {
+    uint64_t u = is_min ? ~k : k;
+    u = (u >> 63) ? (u & 0x7fffffffffffffffull) : ~u;
+    return __longlong_as_double((long long)u);
+}
+
+struct alignas(16) Win {
+    uint64_t key;  // 0 = empty bin
+    uint64_t inv;  // ~index (larger = lower index)
+};
+
+__device__ __forceinline__ bool win_better(uint64_t k, uint64_t i, uint64_t ck, uint64_t ci) {
+    return k > ck || (k == ck && i > ci);
+}
+
+__device__ __forceinline__ void cas128_global(Win *w, uint64_t k, uint64_t i) {
+    uint64_t ck = __ldcg(reinterpret_cast<const unsigned long long *>(&w->key));
+    if (k < ck) return;  // monotone filter: the stored key never decreases
+    uint64_t ci = __ldcg(reinterpret_cast<const unsigned long long *>(&w->inv));
+    while (win_better(k, i, ck, ci)) {
+        uint64_t ok, oi;
+        asm volatile(
+            "{ .reg .b128 c, s, r; mov.b128 c, {%2,%3}; mov.b128 s, {%4,%5};"
+            " atom.global.cas.b128 r, [%6], c, s; mov.b128 {%0,%1}, r; }"
+            : "=l"(ok), "=l"(oi) : "l"(ck), "l"(ci), "l"(k), "l"(i), "l"(w) : "memory");
+        if (ok == ck && oi == ci) return;
+        ck = ok;
+        ci = oi;
+    }
+}
+__device__ __forceinline__ void cas128_shared(Win *w, uint64_t k, uint64_t i) {
+    uint64_t ck = *reinterpret_cast<volatile uint64_t *>(&w->key);
+    if (k < ck) return;
+    uint64_t ci = *reinterpret_cast<volatile uint64_t *>(&w->inv);
+    const uint32_t a = smem_u32(w);
+    while (win_better(k, i, ck, ci)) {
+        uint64_t ok, oi;
+        asm volatile(
+            "{ .reg .b128 c, s, r; mov.b128 c, {%2,%3}; mov.b128 s, {%4,%5};"
+            " atom.shared.cas.b128 r, [%6], c, s; mov.b128 {%0,%1}, r; }"
+            : "=l"(ok), "=l"(oi) : "l"(ck), "l"(ci), "l"(k), "l"(i), "r"(a) : "memory");
+        if (ok == ck && oi == ci) return;
+        ck = ok;
+        ci = oi;
+    }
+}
+
+__device__ __forceinline__ void mul_cas_global(double *addr, double x) {
+    unsigned long long *a = reinterpret_cast<unsigned long long *>(addr);
+    unsigned long long old = __ldcg(a), assumed;
+    do {
+        assumed = old;
+        old = atomicCAS(a, assumed, (unsigned long long)__double_as_longlong(__longlong_as_double((long long)assumed) * x));
+    } while (old != assumed);
+}
+
+struct RbiParams {
+    int64_t n, m, goff;
+    int32_t acc, zero_fill;
+    double *p;        // MUL: [m] product of nonzeros
+    unsigned long long *z;  // MUL: [m] zero count
+    Win *win;         // MIN/MAX: [m]
+};
+
+// ------------------------------------------------------------ init
+template <int OP>
+__global__ void rbi_init(RbiParams P) {
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < P.m; b += (int64_t)gridDim.x * blockDim.x) {
+        if (OP == VJP_MUL) { P.p[b] = 1.0; P.z[b] = 0ull; }
+        else { P.win[b].key = 0ull; P.win[b].inv = 0ull; }
+    }
+}
+
+// ------------------------------------------------------------ forward
+// Every element is visited once (grid-stride over 16-byte index vectors);
+// `visit(b, x, gi)` is called for in-range bins.
+template <class T, class I, class F>
+__device__ __forceinline__ void rbi_stream(const I *__restrict__ inds, const T *__restrict__ as, T *__restrict__ ab,
+                                           const RbiParams &P, F visit) {
+    // warp-uniform trip counts: visitors may use full-warp intrinsics
+    using IV = IdxVec<I>;
+    const int64_t nv = P.n / IV::N;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    const typename IV::V *iv = reinterpret_cast<const typename IV::V *>(inds);
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < nv; base += stride) {
+        const int64_t j = base + lane;
+        const bool in = j < nv;
+        int64_t b[IV::N];
+        double x[IV::N];
+        if (in) {
+            IV::get(__ldcs(iv + j), b);
+#pragma unroll
+            for (int q = 0; q < IV::N; ++q) x[q] = (double)__ldcs(as + j * IV::N + q);
+            if (P.zero_fill) {
+#pragma unroll
+                for (int q = 0; q < IV::N; ++q) __stcs(ab + j * IV::N + q, (T)0);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < IV::N; ++q) { b[q] = -1; x[q] = 0.0; }
+        }
+#pragma unroll
+        for (int q = 0; q < IV::N; ++q) visit(b[q], x[q], P.goff + j * IV::N + q, in && b[q] >= 0 && b[q] < P.m);
+    }
+    // scalar tail (< IV::N elements): warp 0 of block 0, one uniform round
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+        const int64_t e = nv * IV::N + lane;
+        const bool in = e < P.n;
+        const int64_t b = in ? (int64_t)inds[e] : -1;
+        const double x = in ? (double)as[e] : 0.0;
+        if (in && P.zero_fill) ab[e] = (T)0;
+        visit(b, x, P.goff + e, in && b >= 0 && b < P.m);
+    }
+}
+
+// large m: global atomics
+template <class T, class I, int OP>
+__global__ void __launch_bounds__(kBThreads) rbi_fwd_global(const I *__restrict__ inds, const T *__restrict__ as,
+                                                            T *__restrict__ ab, RbiParams P) {
+    const bool is_min = OP == VJP_MIN;
+    rbi_stream<T, I>(inds, as, ab, P, [&](int64_t b, double x, int64_t gi, bool ok) {
+        if (!ok) return;
+        if (OP == VJP_MUL) {
+            if (x == 0.0) atomicAdd(P.z + b, 1ull);
+            else mul_cas_global(P.p + b, x);
+        } else {
+            cas128_global(P.win + b, ord_key(x, is_min), ~(uint64_t)gi);
+        }
+    });
+}
+
+// small m, MIN/MAX: one shared-memory Win[m] per CTA, filtered CAS, then merged
+template <class T, class I, int OP>
+__global__ void __launch_bounds__(kBThreads) rbi_fwd_smem_ext(const I *__restrict__ inds, const T *__restrict__ as,
+                                                              T *__restrict__ ab, RbiParams P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    Win *h = reinterpret_cast<Win *>(smem);
+    const bool is_min = OP == VJP_MIN;
+    for (int64_t b = threadIdx.x; b < P.m; b += blockDim.x) { h[b].key = 0ull; h[b].inv = 0ull; }
+    __syncthreads();
+    rbi_stream<T, I>(inds, as, ab, P, [&](int64_t b, double x, int64_t gi, bool ok) {
+        if (ok) cas128_shared(h + b, ord_key(x, is_min), ~(uint64_t)gi);
+    });
+    __syncthreads();
+    for (int64_t b = threadIdx.x; b < P.m; b += blockDim.x)
+        if (h[b].key) cas128_global(P.win + b, h[b].key, h[b].inv);
+}
+
+// small m, MUL: warp-private histograms (p: double, z: uint32) in shared memory
+template <class T, class I>
+__global__ void __launch_bounds__(kBThreads) rbi_fwd_smem_mul(const I *__restrict__ inds, const T *__restrict__ as,
+                                                              T *__restrict__ ab, RbiParams P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double *hp = reinterpret_cast<double *>(smem);                              // [nw][m]
+    uint32_t *hz = reinterpret_cast<uint32_t *>(smem + sizeof(double) * nw * P.m);  // [nw][m]
+    for (int64_t k = threadIdx.x; k < (int64_t)nw * P.m; k += blockDim.x) { hp[k] = 1.0; hz[k] = 0u; }
+    __syncthreads();
+    double *wp = hp + warp * P.m;
+    uint32_t *wz = hz + warp * P.m;
+    rbi_stream<T, I>(inds, as, ab, P, [&](int64_t b, double x, int64_t, bool ok) {
+        // one round per multiplicity: the lowest pending lane of each bin updates it
+        bool pending = ok;
+        while (__any_sync(0xffffffffu, pending)) {
+            const unsigned key = pending ? (unsigned)b : (0x80000000u | (unsigned)lane);
+            const unsigned same = __match_any_sync(0xffffffffu, key);
+            if (pending && (__ffs(same) - 1) == lane) {
+                if (x == 0.0) wz[b] += 1u;
+                else wp[b] *= x;
+                pending = false;
+            }
+        }
+    });
+    __syncthreads();
+    for (int64_t b = threadIdx.x; b < P.m; b += blockDim.x) {
+        double pr = 1.0;
+        unsigned long long zz = 0;
+        for (int w = 0; w < nw; ++w) {
+            pr *= hp[w * P.m + b];
+            zz += hz[w * P.m + b];
+        }
+        if (zz) atomicAdd(P.z + b, zz);
+        if (pr != 1.0) mul_cas_global(P.p + b, pr);
+    }
+}
+
+// ADD primal histogram (only when hs is requested; atomic adds, order-dependent rounding)
+template <class T, class I>
+__global__ void __launch_bounds__(kBThreads) rbi_add_hist(const I *__restrict__ inds, const T *__restrict__ as, T *hs,
+                                                          RbiParams P) {
+    rbi_stream<T, I>(inds, as, nullptr, P, [&](int64_t b, double x, int64_t, bool ok) {
+        if (ok) atomicAdd(hs + b, (T)x);
+    });
+}
+
+// ------------------------------------------------------------ return
+template <class T>
+struct MulPack {
+    double q;   // hs_bar_b * p_b
+    int64_t z;  // zero count
+};
+
+template <class T>
+__global__ void rbi_mul_prep(const T *__restrict__ hs_bar, const double *__restrict__ p,
+                             const unsigned long long *__restrict__ z, MulPack<T> *pk, int64_t m, T *hs,
+                             int64_t *winners) {
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < m; b += (int64_t)gridDim.x * blockDim.x) {
+        const double pb = p[b];
+        const int64_t zb = (int64_t)z[b];
+        pk[b].q = (double)hs_bar[b] * pb;
+        pk[b].z = zb;
+        if (hs) hs[b] = (T)(zb ? 0.0 : pb);
+        if (winners) winners[b] = zb;
+    }
+}
+
+// ADD (gather) and MUL (three cases) return map
+template <class T, class I, int OP>
+__global__ void __launch_bounds__(kBThreads) rbi_bwd_map(const I *__restrict__ inds, const T *__restrict__ as,
+                                                         const T *__restrict__ hs_bar, const MulPack<T> *__restrict__ pk,
+                                                         T *__restrict__ ab, int64_t n, int64_t m, int acc) {
+    using IV = IdxVec<I>;
+    auto one = [&](int64_t b, int64_t e) {
+        double v = 0.0;
+        bool touch = true;
+        if (b >= 0 && b < m) {
+            if (OP == VJP_ADD) {
+                v = (double)__ldg(hs_bar + b);
+            } else {
+                const MulPack<T> k = pk[b];
+                if (k.z == 0) {
+                    v = k.q / (double)as[e];  // hs_bar_b * y_b / a_i
+                } else {
+                    const bool zero = (double)as[e] == 0.0;
+                    v = (k.z == 1 && zero) ? k.q : 0.0;  // P:1048-1053 per bin
+                    touch = (k.z == 1 && zero);
+                }
+            }
+        } else {
+            touch = false;
+        }
+        if (acc) {
+            if (touch) ab[e] = (T)((double)ab[e] + v);
+        } else {
+            ab[e] = (T)v;
+        }
+    };
+    const int64_t nv = n / IV::N;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const typename IV::V *iv = reinterpret_cast<const typename IV::V *>(inds);
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nv; j += stride) {
+        int64_t b[IV::N];
+        IV::get(__ldcs(iv + j), b);
+#pragma unroll
+        for (int q = 0; q < IV::N; ++q) one(b[q], j * IV::N + q);
+    }
+    if (blockIdx.x == 0)
+        for (int64_t e = nv * IV::N + threadIdx.x; e < n; e += blockDim.x) one((int64_t)inds[e], e);
+}
+
+// MIN/MAX return: scatter hs_bar[b] to the winner of every bin (as_bar was
+// zero-filled by the forward kernel in dense mode)
+template <class T, int OP>
+__global__ void rbi_ext_scatter(const Win *__restrict__ win, const T *__restrict__ hs_bar, T *__restrict__ ab,
+                                int64_t m, int64_t goff, int64_t n, int acc, T *hs, int64_t *winners) {
+    const bool is_min = OP == VJP_MIN;
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < m; b += (int64_t)gridDim.x * blockDim.x) {
+        const Win w = win[b];
+        const int64_t gi = w.key ? (int64_t)~w.inv : -1;
+        if (winners) winners[b] = gi;
+        if (hs) hs[b] = (T)(w.key ? key_val(w.key, is_min) : (is_min ? INFINITY : -INFINITY));
+        if (gi >= goff && gi < goff + n) {
+            T *d = ab + (gi - goff);
+            *d = acc ? (T)((double)*d + (double)hs_bar[b]) : hs_bar[b];
+        }
+    }
+}
+
+// multi-GPU helpers -------------------------------------------------------
+template <int OP>
+__global__ void rbi_export(const RbiParams P, double *bin_val, int64_t *bin_aux) {
+    const bool is_min = OP == VJP_MIN;
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < P.m; b += (int64_t)gridDim.x * blockDim.x) {
+        if (OP == VJP_MUL) {
+            bin_val[b] = P.p[b];
+            bin_aux[b] = (int64_t)P.z[b];
+        } else {
+            const Win w = P.win[b];
+            bin_val[b] = w.key ? key_val(w.key, is_min) : (is_min ? INFINITY : -INFINITY);
+            bin_aux[b] = w.key ? (int64_t)~w.inv : INT64_MAX;
+        }
+    }
+}
+__global__ void rbi_select(int64_t m, const double *gval, const double *lval, int64_t *aux) {
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < m; b += (int64_t)gridDim.x * blockDim.x)
+        if (!(lval[b] == gval[b])) aux[b] = INT64_MAX;  // IEEE ==: -0.0 ties +0.0
+}
+template <class T>
+__global__ void rbi_mul_prep_ext(const T *__restrict__ hs_bar, const double *__restrict__ bin_val,
+                                 const int64_t *__restrict__ bin_aux, MulPack<T> *pk, int64_t m) {
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < m; b += (int64_t)gridDim.x * blockDim.x) {
+        pk[b].q = (double)hs_bar[b] * bin_val[b];
+        pk[b].z = bin_aux[b];
+    }
+}
+// dense MIN/MAX finish over a shard: as_bar_i = hs_bar[b_i] iff i is the bin's global winner
+template <class T, class I>
+__global__ void __launch_bounds__(kBThreads) rbi_ext_gather(const I *__restrict__ inds, const T *__restrict__ hs_bar,
+                                                            const int64_t *__restrict__ bin_aux, T *__restrict__ ab,
+                                                            int64_t n, int64_t m, int64_t goff, int acc) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = (int64_t)inds[e];
+        const bool won = b >= 0 && b < m && bin_aux[b] == goff + e;
+        if (acc) {
+            if (won) ab[e] = (T)((double)ab[e] + (double)hs_bar[b]);
+        } else {
+            ab[e] = won ? hs_bar[b] : (T)0;
+        }
+    }
+}
+
+}  // namespace vjpk
+
+// =============================================================================
+// host side
+// =============================================================================
+namespace {
+using namespace vjpk;
+
+constexpr size_t kSmemCap = 200 * 1024;
+
+bool op_ok(vjp_op op) { return op == VJP_ADD || op == VJP_MUL || op == VJP_MIN || op == VJP_MAX; }
+
+struct BLayout {
+    size_t p, z, win, pk, total;
+};
+BLayout blayout(int64_t m) {
+    BLayout L{};
+    size_t off = 0;
+    L.p = off; off += vjph::align256(sizeof(double) * (size_t)m);
+    L.z = off; off += vjph::align256(sizeof(unsigned long long) * (size_t)m);
+    L.win = off; off += vjph::align256(sizeof(Win) * (size_t)m);
+    L.pk = off; off += vjph::align256(16 * (size_t)m);
+    L.total = off;
+    return L;
+}
+
+int grid_for(int64_t work, int per_sm) {
+    int64_t g = (work + kBThreads - 1) / kBThreads;
+    int64_t cap = (int64_t)vjph::sm_count() * per_sm;
+    if (g > cap) g = cap;
+    return (int)(g < 1 ? 1 : g);
+}
+
+RbiParams params(int64_t n, int64_t m, int64_t goff, void *ws, unsigned flags, int zero_fill) {
+    BLayout L = blayout(m);
+    unsigned char *w = static_cast<unsigned char *>(ws);
+    RbiParams P{};
+    P.n = n;
+    P.m = m;
+    P.goff = goff;
+    P.acc = (flags & VJP_ACCUMULATE) ? 1 : 0;
+    P.zero_fill = zero_fill;
+    P.p = reinterpret_cast<double *>(w + L.p);
+    P.z = reinterpret_cast<unsigned long long *>(w + L.z);
+    P.win = reinterpret_cast<Win *>(w + L.win);
+    return P;
+}
+
+// forward histogram (MUL / MIN / MAX), init included
+template <class T, class I, int OP>
+vjp_status forward(const I *inds, const T *as, T *ab, const RbiParams &P, cudaStream_t s) {
+    rbi_init<OP><<<grid_for(P.m, 4), kBThreads, 0, s>>>(P);
+    vjph::count_launch();
+    const int nvec = (int)(16 / sizeof(I));
+    const int64_t work = P.n / nvec + 1;
+    if (OP == VJP_MUL) {
+        const size_t sm = (size_t)(kBThreads / 32) * (size_t)P.m * (sizeof(double) + sizeof(uint32_t));
+        if (sm <= kSmemCap) {
+            auto k = rbi_fwd_smem_mul<T, I>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            int occ = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kBThreads, sm);
+            k<<<grid_for(work, occ < 1 ? 1 : occ), kBThreads, sm, s>>>(inds, as, ab, P);
+        } else {
+            rbi_fwd_global<T, I, OP><<<grid_for(work, 8), kBThreads, 0, s>>>(inds, as, ab, P);
+        }
+    } else {
+        const size_t sm = sizeof(Win) * (size_t)P.m;
+        if (sm <= kSmemCap && P.m <= 16384) {
+            auto k = rbi_fwd_smem_ext<T, I, OP>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            int occ = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kBThreads, sm);
+            k<<<grid_for(work, occ < 1 ? 1 : occ), kBThreads, sm, s>>>(inds, as, ab, P);
+        } else {
+            rbi_fwd_global<T, I, OP><<<grid_for(work, 8), kBThreads, 0, s>>>(inds, as, ab, P);
+        }
+    }
+    vjph::count_launch();
+    return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+}
+
+template <class T, class I>
+vjp_status run_full(vjp_op op, int64_t n, int64_t m, const void *inds_, const void *as_, const void *hsb_, void *ab_,
+                    void *hs_, int64_t *winners, void *ws, cudaStream_t s, unsigned flags) {
+    const I *inds = static_cast<const I *>(inds_);
+    const T *as = static_cast<const T *>(as_);
+    const T *hsb = static_cast<const T *>(hsb_);
+    T *ab = static_cast<T *>(ab_);
+    T *hs = static_cast<T *>(hs_);
+    const int acc = (flags & VJP_ACCUMULATE) ? 1 : 0;
+    const int nvec = (int)(16 / sizeof(I));
+    if (op == VJP_ADD) {
+        if (hs) {
+            // primal histogram only on request: atomic adds (order-dependent rounding)
+            if (cudaMemsetAsync(hs, 0, sizeof(T) * (size_t)m, s) != cudaSuccess) return VJP_ECUDA;
+            RbiParams P = params(n, m, 0, ws, 0, 0);
+            rbi_add_hist<T, I><<<grid_for(n / nvec + 1, 8), kBThreads, 0, s>>>(inds, as, hs, P);
+            vjph::count_launch();
+        }
+        rbi_bwd_map<T, I, VJP_ADD><<<grid_for(n / nvec + 1, 8), kBThreads, 0, s>>>(inds, as, hsb, nullptr, ab, n, m, acc);
+        vjph::count_launch();
+        if (cudaGetLastError() != cudaSuccess) return VJP_ECUDA;
+        if (winners && cudaMemsetAsync(winners, 0xff, sizeof(int64_t) * (size_t)m, s) != cudaSuccess) return VJP_ECUDA;
+        return VJP_OK;
+    }
+    RbiParams P = params(n, m, 0, ws, flags, (op != VJP_MUL && !acc) ? 1 : 0);
+    vjp_status st = VJP_OK;
+    if (op == VJP_MUL) st = forward<T, I, VJP_MUL>(inds, as, ab, P, s);
+    if (op == VJP_MIN) st = forward<T, I, VJP_MIN>(inds, as, ab, P, s);
+    if (op == VJP_MAX) st = forward<T, I, VJP_MAX>(inds, as, ab, P, s);
+    if (st != VJP_OK) return st;
+    BLayout L = blayout(m);
+    if (op == VJP_MUL) {
+        MulPack<T> *pk = reinterpret_cast<MulPack<T> *>(static_cast<unsigned char *>(ws) + L.pk);
+        rbi_mul_prep<T><<<grid_for(m, 4), kBThreads, 0, s>>>(hsb, P.p, P.z, pk, m, hs, winners);
+        rbi_bwd_map<T, I, VJP_MUL><<<grid_for(n / nvec + 1, 8), kBThreads, 0, s>>>(inds, as, hsb, pk, ab, n, m, acc);
+        vjph::count_launch(2);
+    } else if (op == VJP_MIN) {
+        rbi_ext_scatter<T, VJP_MIN><<<grid_for(m, 4), kBThreads, 0, s>>>(P.win, hsb, ab, m, 0, n, acc, hs, winners);
+        vjph::count_launch();
+    } else {
+        rbi_ext_scatter<T, VJP_MAX><<<grid_for(m, 4), kBThreads, 0, s>>>(P.win, hsb, ab, m, 0, n, acc, hs, winners);
+        vjph::count_launch();
+    }
+    return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+}
+
+template <class T, class I>
+vjp_status run_partial(vjp_op op, int64_t n, int64_t m, int64_t goff, const void *inds, const void *as, void *ws,
+                       double *bin_val, int64_t *bin_aux, cudaStream_t s) {
+    RbiParams P = params(n, m, goff, ws, 0, 0);
+    vjp_status st = VJP_OK;
+    const I *ix = static_cast<const I *>(inds);
+    const T *a = static_cast<const T *>(as);
+    if (op == VJP_MUL) st = forward<T, I, VJP_MUL>(ix, a, nullptr, P, s);
+    if (op == VJP_MIN) st = forward<T, I, VJP_MIN>(ix, a, nullptr, P, s);
+    if (op == VJP_MAX) st = forward<T, I, VJP_MAX>(ix, a, nullptr, P, s);
+    if (st != VJP_OK) return st;
+    if (op == VJP_MUL) rbi_export<VJP_MUL><<<grid_for(m, 4), kBThreads, 0, s>>>(P, bin_val, bin_aux);
+    if (op == VJP_MIN) rbi_export<VJP_MIN><<<grid_for(m, 4), kBThreads, 0, s>>>(P, bin_val, bin_aux);
+    if (op == VJP_MAX) rbi_export<VJP_MAX><<<grid_for(m, 4), kBThreads, 0, s>>>(P, bin_val, bin_aux);
+    vjph::count_launch();
+    return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+}
+
+template <class T, class I>
+vjp_status run_finish(vjp_op op, int64_t n, int64_t m, int64_t goff, const void *inds_, const void *as_,
+                      const void *hsb_, void *ab_, const double *bin_val, const int64_t *bin_aux, void *ws,
+                      cudaStream_t s, unsigned flags) {
+    const I *inds = static_cast<const I *>(inds_);
+    const T *as = static_cast<const T *>(as_);
+    const T *hsb = static_cast<const T *>(hsb_);
+    T *ab = static_cast<T *>(ab_);
+    const int acc = (flags & VJP_ACCUMULATE) ? 1 : 0;
+    const int nvec = (int)(16 / sizeof(I));
+    if (op == VJP_ADD) {
+        rbi_bwd_map<T, I, VJP_ADD><<<grid_for(n / nvec + 1, 8), kBThreads, 0, s>>>(inds, as, hsb, nullptr, ab, n, m, acc);
+    } else if (op == VJP_MUL) {
+        BLayout L = blayout(m);
+        MulPack<T> *pk = reinterpret_cast<MulPack<T> *>(static_cast<unsigned char *>(ws) + L.pk);
+        rbi_mul_prep_ext<T><<<grid_for(m, 4), kBThreads, 0, s>>>(hsb, bin_val, bin_aux, pk, m);
+        vjph::count_launch();
+        rbi_bwd_map<T, I, VJP_MUL><<<grid_for(n / nvec + 1, 8), kBThreads, 0, s>>>(inds, as, hsb, pk, ab, n, m, acc);
+    } else {
+        rbi_ext_gather<T, I><<<grid_for(n, 8), kBThreads, 0, s>>>(inds, hsb, bin_aux, ab, n, m, goff, acc);
+    }
+    vjph::count_launch();
+    return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+}
+
+vjp_status common_check(vjp_op op, vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, const void *inds,
+                        const void *as, const void *hs_bar) {
+    if (op == VJP_LINREC || op == VJP_MAT2) return VJP_EUNSUPPORTED;  // no rule in the paper
+    if (!op_ok(op) || (dtype != VJP_F32 && dtype != VJP_F64) || (itype != VJP_I32 && itype != VJP_I64)) return VJP_EINVAL;
+    if (n < 0 || m < 1) return VJP_EINVAL;
+    if (n == 0) return VJP_OK;
+    if (!inds || !hs_bar || (!as && op != VJP_ADD)) return VJP_EINVAL;
+    const void *ps[3] = {inds, as, hs_bar};
+    for (const void *p : ps)
+        if (p && !vjph::aligned16(p)) return VJP_EALIGN;
+    return VJP_OK;
+}
+
+#define RBI_DISPATCH(FN, ...)                                                                        \
+    (dtype == VJP_F64 ? (itype == VJP_I32 ? FN<double, int32_t>(__VA_ARGS__) : FN<double, int64_t>(__VA_ARGS__)) \
+                      : (itype == VJP_I32 ? FN<float, int32_t>(__VA_ARGS__) : FN<float, int64_t>(__VA_ARGS__)))
+}  // namespace
+
+extern "C" {
+
+size_t vjp_reduce_by_index_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_t n, int64_t m) {
+    (void)dtype;
+    (void)n;
+    if (!op_ok(op) || m < 1) return 0;
+    if (op == VJP_ADD) return 0;
+    return blayout(m).total;
+}
+
+vjp_status vjp_reduce_by_index(vjp_op op, vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, const void *inds,
+                               const void *as, const void *hs_bar, void *as_bar, void *hs, int64_t *winners, void *ws,
+                               size_t ws_bytes, vjp_stream_t stream, unsigned flags) {
+    vjp_status st = common_check(op, dtype, itype, n, m, inds, as, hs_bar);
+    if (st != VJP_OK || n == 0) return st;
+    if (!as_bar) return VJP_EINVAL;
+    if (!vjph::aligned16(as_bar)) return VJP_EALIGN;
+    if (op == VJP_ADD && hs && !as) return VJP_EINVAL;  // the primal sum needs `as`
+    const size_t need = vjp_reduce_by_index_workspace_bytes(op, dtype, n, m);
+    if (ws_bytes < need || (need && !ws)) return VJP_EWORKSPACE;
+    if (ws && !vjph::aligned16(ws)) return VJP_EALIGN;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    return RBI_DISPATCH(run_full, op, n, m, inds, as, hs_bar, as_bar, hs, winners, ws, s, flags);
+}
+
+vjp_status vjp_reduce_by_index_partial(vjp_op op, vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m,
+                                       const void *inds, const void *as, void *ws, size_t ws_bytes,
+                                       const vjp_shard *shard, double *bin_val, int64_t *bin_aux,
+                                       vjp_stream_t stream) {
+    if (!shard) return VJP_EINVAL;
+    if (op == VJP_ADD) return op_ok(op) ? VJP_OK : VJP_EINVAL;
+    vjp_status st = common_check(op, dtype, itype, n, m, inds, as, inds);
+    if (st != VJP_OK) return st;
+    if (!bin_val || !bin_aux) return VJP_EINVAL;
+    if (ws_bytes < blayout(m).total || !ws) return VJP_EWORKSPACE;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (n == 0) {
+        // empty shard: neutral per-bin state
+        RbiParams P = params(0, m, shard->global_offset, ws, 0, 0);
+        if (op == VJP_MUL) { rbi_init<VJP_MUL><<<grid_for(m, 4), kBThreads, 0, s>>>(P); rbi_export<VJP_MUL><<<grid_for(m, 4), kBThreads, 0, s>>>(P, bin_val, bin_aux); }
+        if (op == VJP_MIN) { rbi_init<VJP_MIN><<<grid_for(m, 4), kBThreads, 0, s>>>(P); rbi_export<VJP_MIN><<<grid_for(m, 4), kBThreads, 0, s>>>(P, bin_val, bin_aux); }
+        if (op == VJP_MAX) { rbi_init<VJP_MAX><<<grid_for(m, 4), kBThreads, 0, s>>>(P); rbi_export<VJP_MAX><<<grid_for(m, 4), kBThreads, 0, s>>>(P, bin_val, bin_aux); }
+        vjph::count_launch(2);
+        return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+    }
+    return RBI_DISPATCH(run_partial, op, n, m, shard->global_offset, inds, as, ws, bin_val, bin_aux, s);
+}
+
+vjp_status vjp_reduce_by_index_select(vjp_op op, int64_t m, const double *bin_val_global, const double *bin_val_local,
+                                      int64_t *bin_aux, vjp_stream_t stream) {
+    if ((op != VJP_MIN && op != VJP_MAX) || m < 1 || !bin_val_global || !bin_val_local || !bin_aux) return VJP_EINVAL;
+    rbi_select<<<grid_for(m, 4), kBThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(m, bin_val_global,
+                                                                                         bin_val_local, bin_aux);
+    vjph::count_launch();
+    return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+}
+
+vjp_status vjp_reduce_by_index_finish(vjp_op op, vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m,
+                                      const void *inds, const void *as, const void *hs_bar, void *as_bar,
+                                      const double *bin_val, const int64_t *bin_aux, void *ws, size_t ws_bytes,
+                                      const vjp_shard *shard, vjp_stream_t stream, unsigned flags) {
+    if (!shard) return VJP_EINVAL;
+    vjp_status st = common_check(op, dtype, itype, n, m, inds, as, hs_bar);
+    if (st != VJP_OK || n == 0) return st;
+    if (!as_bar) return VJP_EINVAL;
+    if (!vjph::aligned16(as_bar)) return VJP_EALIGN;
+    if (op != VJP_ADD && (!bin_val || !bin_aux)) return VJP_EINVAL;
+    const size_t need = vjp_reduce_by_index_workspace_bytes(op, dtype, n, m);
+    if (ws_bytes < need || (need && !ws)) return VJP_EWORKSPACE;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    return RBI_DISPATCH(run_finish, op, n, m, shard->global_offset, inds, as, hs_bar, as_bar, bin_val, bin_aux, ws,
+                        s, flags);
+}
+
+}  // extern "C"

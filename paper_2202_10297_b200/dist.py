@@ -117,9 +117,9 @@ def reduce_by_index(op, inds: torch.Tensor, as_: torch.Tensor | None, hs_bar: to
     s = _stream(dev)
     bin_val = torch.empty(m, dtype=torch.float64, device=dev)
     bin_aux = torch.empty(m, dtype=torch.int64, device=dev)
-    if op not in ("add", 1):
-        ws = workspace(L.vjp_reduce_by_index_workspace_bytes(o, dt, n, m), dev)
-        nbytes = 0 if ws is None else ws.numel()
+    ws = workspace(L.vjp_reduce_by_index_workspace_bytes(o, dt, n, m), dev)
+    nbytes = 0 if ws is None else ws.numel()
+    if o != 1:  # ADD needs no exchange: hs_bar is replicated
         _check(L.vjp_reduce_by_index_partial(o, dt, it, n, m, _p(inds), _p(as_), _p(ws), nbytes, sh, _p(bin_val),
                                              _p(bin_aux), s), "vjp_reduce_by_index_partial")
         if sh.world > 1:
@@ -133,6 +133,6 @@ def reduce_by_index(op, inds: torch.Tensor, as_: torch.Tensor | None, hs_bar: to
                        "vjp_reduce_by_index_select")
                 dist.all_reduce(bin_aux, op=dist.ReduceOp.MIN, group=group)
     _check(L.vjp_reduce_by_index_finish(o, dt, it, n, m, _p(inds), _p(as_), _p(hs_bar), _p(ab), _p(bin_val),
-                                        _p(bin_aux), sh, s, ACCUMULATE if accumulate else 0),
+                                        _p(bin_aux), _p(ws), nbytes, sh, s, ACCUMULATE if accumulate else 0),
            "vjp_reduce_by_index_finish")
     return ab

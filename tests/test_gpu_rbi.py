@@ -1,0 +1,100 @@
+"""GPU parity of vjp_reduce_by_index (sec 5.1.2) against the oracle.
+
+Per-bin winners (MIN/MAX, lowest index on ties) and zero counts (MUL) are
+compared bit-exactly; adjoints within the north_star tolerance (ADD and
+MIN/MAX adjoints are copies of hs_bar, so bit-exact).  m spans the shared-
+memory and the global-atomic forward paths.  Config 4 (n = 2^28, m = 10^3 and
+10^6) runs at full size in the `slow` cases."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from _parity import assert_close
+
+pytestmark = pytest.mark.gpu
+vjp = pytest.importorskip("paper_2202_10297_b200")
+DEV = "cuda"
+TD = {np.float32: torch.float32, np.float64: torch.float64}
+
+
+def run(op, n, m, dt, it=torch.int32, oob=False, skew=False):
+    inds, a, hb = synth.rbi_inputs(n, m, op, dtype=TD[dt], itype=it, skew=skew)
+    if oob and n > 4:
+        inds[1] = -1
+        inds[3] = m + 5
+    ref_ab, ref_hs, ref_win, ref_z = oracle.vjp_reduce_by_index(op, inds.numpy(), a.numpy(), hb.numpy())
+    ab, hs, win = vjp.reduce_by_index(op, inds.to(DEV), a.to(DEV), hb.to(DEV), want_hs=True)
+    ab = ab.cpu().numpy()
+    if op in ("min", "max"):
+        assert np.array_equal(win.cpu().numpy(), ref_win), "winner indices differ"
+        assert np.array_equal(ab, ref_ab)
+        occupied = ref_win >= 0
+        assert np.array_equal(hs.cpu().numpy()[occupied], ref_hs[occupied])
+    elif op == "mul":
+        assert np.array_equal(win.cpu().numpy(), ref_z), "zero counts differ"
+        assert_close(ab, ref_ab, dt, what=f"rbi mul n={n} m={m}")
+    else:
+        assert np.array_equal(ab, ref_ab)
+        assert_close(hs.cpu().numpy(), ref_hs, dt, scale=np.full(m, max(1.0, n / m)), what="primal sum")
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32], ids=["f64", "f32"])
+@pytest.mark.parametrize("op", ["add", "mul", "min", "max"])
+def test_rbi_sizes(op, dt):
+    for n, m in [(1, 1), (5, 3), (1000, 1), (4097, 17), (100_003, 1000), (100_003, 2100), (300_001, 4096),
+                 (300_001, 20_000), (1 << 20, 1_000_000)]:
+        run(op, n, m, dt, oob=True)
+
+
+@pytest.mark.parametrize("op", ["add", "mul", "max"])
+def test_rbi_int64_and_skew(op):
+    run(op, 200_001, 1000, np.float64, it=torch.int64)
+    run(op, 200_001, 50_000, np.float64, it=torch.int64, skew=True)
+
+
+def test_rbi_golden_g5_g6():
+    inds = torch.tensor([0, 1, 0, 1, 2, 2], dtype=torch.int32)
+    a = torch.tensor([2, 0, 3, 5, 0, 0], dtype=torch.float64)
+    got = vjp.reduce_by_index("mul", inds.to(DEV), a.to(DEV), torch.tensor([1.0, 10, 100], dtype=torch.float64, device=DEV))
+    assert got.cpu().tolist() == [3, 50, 2, 0, 0, 0]
+    inds = torch.tensor([0, 1, 0, 1, 0], dtype=torch.int32)
+    a = torch.tensor([3, 5, 3, -1, 2], dtype=torch.float64)
+    got = vjp.reduce_by_index("max", inds.to(DEV), a.to(DEV), torch.tensor([7.0, 9], dtype=torch.float64, device=DEV))
+    assert got.cpu().tolist() == [7, 9, 0, 0, 0]
+
+
+def test_rbi_accumulate():
+    n, m = 100_003, 777
+    for op in ("add", "mul", "max"):
+        inds, a, hb = synth.rbi_inputs(n, m, op)
+        base = synth.uniform(n, 700, dtype=torch.float64)
+        ref = oracle.vjp_reduce_by_index(op, inds.numpy(), a.numpy(), hb.numpy(), out=base.numpy().copy(),
+                                         accumulate=True)[0]
+        out = base.to(DEV)
+        vjp.reduce_by_index(op, inds.to(DEV), a.to(DEV), hb.to(DEV), out=out, accumulate=True)
+        assert_close(out.cpu().numpy(), ref, np.float64, what=f"acc {op}")
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("m", [1000, 1_000_000])
+@pytest.mark.parametrize("op", ["add", "mul", "max"])
+def test_config4_full_size(op, m):
+    """config 4: n = 2^28, f64 values, int32 bins, k-means-shaped (uniform bins)."""
+    n = 1 << 28
+    inds, a, hb = synth.rbi_inputs(n, m, op, device=DEV)
+    ab, hs, win = vjp.reduce_by_index(op, inds, a, hb, want_hs=True)
+    ref_ab, ref_hs, ref_win, ref_z = oracle.vjp_reduce_by_index(op, inds.cpu().numpy(), a.cpu().numpy(),
+                                                                hb.cpu().numpy())
+    got = ab.cpu().numpy()
+    if op == "max":
+        assert np.array_equal(win.cpu().numpy(), ref_win)
+        assert np.array_equal(got, ref_ab)
+    elif op == "mul":
+        assert np.array_equal(win.cpu().numpy(), ref_z)
+        assert_close(got, ref_ab, np.float64, what=f"config4 mul m={m}")
+    else:
+        assert np.array_equal(got, ref_ab)
