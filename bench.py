@@ -287,6 +287,73 @@ def run_ours(args):
     return 0
 
 
+def run_extra(args):
+    """Extra lines for DESIGN.md/BASELINE.md (not the headline): each vjp call of
+    configs 1-4 timed alone with CUDA events (median over steps)."""
+    import torch
+
+    import paper_2202_10297_b200 as vjp
+    import synth
+
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    vjp.lib()
+    peak, peak_src = peaks()
+    cases = []
+    N30, N28, N26 = 1 << 30, 1 << 28, 1 << 26
+    w = args.workload
+    if w in ("scan_add", "all"):
+        yb = synth.scan_add_seed(N30, device=dev)
+        out = torch.empty_like(yb)
+        cases.append(("scan ADD f64 n=2^30 (target)", N30, 16 * N30,
+                      lambda yb=yb, out=out: vjp.scan("add", yb, out=out)))
+        cases.append(("scan ADD f64 n=2^30 look-back kernels", N30, 16 * N30,
+                      lambda yb=yb, out=out: vjp.scan("add", yb, out=out, lookback=True)))
+    if w in ("scan_linrec30", "all"):
+        a, yb2 = synth.linrec_inputs(N30, device=dev)
+        out2 = torch.empty_like(yb2)
+        cases.append(("scan LINREC f64 n=2^30", N30, 64 * N30,
+                      lambda yb2=yb2, a=a, out2=out2: vjp.scan("linrec", yb2, a, out=out2)))
+    if w in ("reduce", "all"):
+        for z in ("none", "one", "two", "sparse"):
+            a = synth.mul_inputs(N30, zeros=z, dtype=torch.float32, device=dev)
+            o = torch.empty_like(a)
+            nb = (12 if z == "none" else 8) * N30
+            cases.append((f"reduce MUL f32 n=2^30 zeros={z}", N30, nb,
+                          (lambda a=a, o=o: vjp.reduce("mul", a, 1.0, out=o))))
+        a = synth.min_inputs(N30, dtype=torch.float32, device=dev)
+        o = torch.empty_like(a)
+        cases.append(("reduce MIN f32 n=2^30 dense", N30, 8 * N30,
+                      lambda a=a, o=o: vjp.reduce("min", a, 1.5, out=o)))
+        cases.append(("reduce MIN f32 n=2^30 accumulate", N30, 4 * N30,
+                      lambda a=a, o=o: vjp.reduce("min", a, 1.5, out=o, accumulate=True)))
+    if w in ("rbi", "all"):
+        for m in (1000, 1_000_000):
+            for op, nb in (("add", 12), ("mul", 32), ("max", 20)):
+                inds, a, hb = synth.rbi_inputs(N28, m, op, device=dev)
+                o = torch.empty(N28, dtype=torch.float64, device=dev)
+                cases.append((f"rbi {op.upper()} f64 n=2^28 m={m}", N28, nb * N28,
+                              (lambda op=op, inds=inds, a=a, hb=hb, o=o: vjp.reduce_by_index(op, inds, a, hb, out=o))))
+    for name, n, nbytes, fn in cases:
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = statistics.median(ts)
+        print(json.dumps({"extra": name, "n": n, "ms": ms, "elements_per_s": n / (ms * 1e-3),
+                          "alg_bytes": nbytes, "alg_gbs": nbytes / (ms * 1e-3) / 1e9,
+                          "frac_of_peak": nbytes / (ms * 1e-3) / 1e9 / peak, "peak": peak,
+                          "min_ms": min(ts)}), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -296,11 +363,16 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override elements per op per GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="config2",
+                    choices=["config2", "scan_add", "scan_linrec30", "reduce", "rbi", "all"],
+                    help="config2 = the headline line; the others print per-call extra lines")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload != "config2":
+        return run_extra(args)
     return run_ours(args)
 
 

@@ -109,6 +109,7 @@ __device__ __forceinline__ void mul_cas_global(double *addr, double x) {
 struct RbiParams {
     int64_t n, m, goff;
     int32_t acc, zero_fill;
+    int32_t v256, pad;  // value arrays 32-byte aligned: 256-bit accesses
     double *p;        // MUL: [m] product of nonzeros
     unsigned long long *z;  // MUL: [m] zero count
     Win *win;         // MIN/MAX: [m]
@@ -123,46 +124,120 @@ __global__ void rbi_init(RbiParams P) {
     }
 }
 
+// ------------------------------------------------------------ element I/O
+// A lane owns 4 consecutive elements per "slab" (a warp covers 128): bins by
+// one 16-byte (int32) or two 16-byte (int64) loads, values by one (f32) or two
+// (f64) 16-byte loads, zero-fill by 16-byte stores — lane-contiguous and
+// read-only cached, so every DRAM sector is fetched once.
+// streamed arrays are touched once: L2 evict_first so they do not push the
+// per-bin state / hs_bar (re-used, L2 resident) out of L2
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void ld_bins4(const int32_t *p, int64_t e, int64_t *b, uint64_t pol) {
+    int x, y, z, w;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "l"(p + e), "l"(pol));
+    b[0] = x; b[1] = y; b[2] = z; b[3] = w;
+}
+__device__ __forceinline__ void ld_bins4(const int64_t *p, int64_t e, int64_t *b, uint64_t pol) {
+    long long x, y, z, w;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s64 {%0,%1}, [%2], %3;"
+                 : "=l"(x), "=l"(y) : "l"(p + e), "l"(pol));
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s64 {%0,%1}, [%2], %3;"
+                 : "=l"(z), "=l"(w) : "l"(p + e + 2), "l"(pol));
+    b[0] = x; b[1] = y; b[2] = z; b[3] = w;
+}
+// f64: one 256-bit access per lane (a whole 32-byte sector); requires 32-byte
+// aligned arrays (checked on the host, else two 128-bit accesses)
+__device__ __forceinline__ void ld_vals4(const double *p, int64_t e, double *x, uint64_t pol, bool v256) {
+    if (v256) {
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=d"(x[0]), "=d"(x[1]), "=d"(x[2]), "=d"(x[3]) : "l"(p + e), "l"(pol));
+    } else {
+        asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(x[0]), "=d"(x[1]) : "l"(p + e), "l"(pol));
+        asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(x[2]), "=d"(x[3]) : "l"(p + e + 2), "l"(pol));
+    }
+}
+__device__ __forceinline__ void ld_vals4(const float *p, int64_t e, double *x, uint64_t pol, bool) {
+    float a, b, c, d;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "l"(p + e), "l"(pol));
+    x[0] = a; x[1] = b; x[2] = c; x[3] = d;
+}
+__device__ __forceinline__ void st_vals4(double *p, int64_t e, const double *x, uint64_t pol, bool v256) {
+    if (v256) {
+        asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f64 [%0], {%1,%2,%3,%4}, %5;"
+                     ::"l"(p + e), "d"(x[0]), "d"(x[1]), "d"(x[2]), "d"(x[3]), "l"(pol) : "memory");
+    } else {
+        asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(p + e), "d"(x[0]), "d"(x[1]), "l"(pol) : "memory");
+        asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(p + e + 2), "d"(x[2]), "d"(x[3]), "l"(pol) : "memory");
+    }
+}
+__device__ __forceinline__ void st_vals4(float *p, int64_t e, const double *x, uint64_t pol, bool) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;"
+                 ::"l"(p + e), "f"((float)x[0]), "f"((float)x[1]), "f"((float)x[2]), "f"((float)x[3]), "l"(pol) : "memory");
+}
+// plain (cached) loads of the accumulate input
+__device__ __forceinline__ void ld_acc4(const double *p, int64_t e, double *x) {
+    double2 v0 = reinterpret_cast<const double2 *>(p + e)[0], v1 = reinterpret_cast<const double2 *>(p + e)[1];
+    x[0] = v0.x; x[1] = v0.y; x[2] = v1.x; x[3] = v1.y;
+}
+__device__ __forceinline__ void ld_acc4(const float *p, int64_t e, double *x) {
+    float4 v = *reinterpret_cast<const float4 *>(p + e);
+    x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+}
+
 // ------------------------------------------------------------ forward
-// Every element is visited once (grid-stride over 16-byte index vectors);
-// `visit(b, x, gi)` is called for in-range bins.
+// Every element is visited once; `visit(b, x, gi, ok)` is called by all 32
+// lanes of a warp together (warp-uniform trip counts), ok = in-range bin.
 template <class T, class I, class F>
 __device__ __forceinline__ void rbi_stream(const I *__restrict__ inds, const T *__restrict__ as, T *__restrict__ ab,
                                            const RbiParams &P, F visit) {
-    // warp-uniform trip counts: visitors may use full-warp intrinsics
-    using IV = IdxVec<I>;
-    const int64_t nv = P.n / IV::N;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t ns = P.n / 128;  // full slabs
     const int lane = threadIdx.x & 31;
-    const typename IV::V *iv = reinterpret_cast<const typename IV::V *>(inds);
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < nv; base += stride) {
-        const int64_t j = base + lane;
-        const bool in = j < nv;
-        int64_t b[IV::N];
-        double x[IV::N];
-        if (in) {
-            IV::get(__ldcs(iv + j), b);
-#pragma unroll
-            for (int q = 0; q < IV::N; ++q) x[q] = (double)__ldcs(as + j * IV::N + q);
-            if (P.zero_fill) {
-#pragma unroll
-                for (int q = 0; q < IV::N; ++q) __stcs(ab + j * IV::N + q, (T)0);
-            }
-        } else {
-#pragma unroll
-            for (int q = 0; q < IV::N; ++q) { b[q] = -1; x[q] = 0.0; }
+    const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const uint64_t pol = policy_evict_first();
+    // register double-buffering: the next slab's loads are in flight while
+    // the current slab's bins are being updated
+    int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int64_t b[4], bn[4];
+    double x[4], xn[4];
+    if (sl < ns) {
+        ld_bins4(inds, sl * 128 + lane * 4, b, pol);
+        ld_vals4(as, sl * 128 + lane * 4, x, pol, P.v256);
+    }
+    for (; sl < ns; sl += wstride) {
+        const int64_t e = sl * 128 + lane * 4;
+        const int64_t sn = sl + wstride;
+        if (sn < ns) {
+            ld_bins4(inds, sn * 128 + lane * 4, bn, pol);
+            ld_vals4(as, sn * 128 + lane * 4, xn, pol, P.v256);
+        }
+        if (P.zero_fill) {
+            const double z[4] = {0.0, 0.0, 0.0, 0.0};
+            st_vals4(ab, e, z, pol, P.v256);
         }
 #pragma unroll
-        for (int q = 0; q < IV::N; ++q) visit(b[q], x[q], P.goff + j * IV::N + q, in && b[q] >= 0 && b[q] < P.m);
+        for (int q = 0; q < 4; ++q) visit(b[q], x[q], P.goff + e + q, b[q] >= 0 && b[q] < P.m);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            b[q] = bn[q];
+            x[q] = xn[q];
+        }
     }
-    // scalar tail (< IV::N elements): warp 0 of block 0, one uniform round
+    // tail (< 128 elements): warp 0 of block 0, warp-uniform rounds
     if (blockIdx.x == 0 && threadIdx.x < 32) {
-        const int64_t e = nv * IV::N + lane;
-        const bool in = e < P.n;
-        const int64_t b = in ? (int64_t)inds[e] : -1;
-        const double x = in ? (double)as[e] : 0.0;
-        if (in && P.zero_fill) ab[e] = (T)0;
-        visit(b, x, P.goff + e, in && b >= 0 && b < P.m);
+        for (int64_t e0 = ns * 128; e0 < P.n; e0 += 32) {
+            const int64_t e = e0 + lane;
+            const bool in = e < P.n;
+            const int64_t bb = in ? (int64_t)inds[e] : -1;
+            const double xx = in ? (double)as[e] : 0.0;
+            if (in && P.zero_fill) ab[e] = (T)0;
+            visit(bb, xx, P.goff + e, in && bb >= 0 && bb < P.m);
+        }
     }
 }
 
@@ -199,29 +274,34 @@ __global__ void __launch_bounds__(kBThreads) rbi_fwd_smem_ext(const I *__restric
         if (h[b].key) cas128_global(P.win + b, h[b].key, h[b].inv);
 }
 
-// small m, MUL: warp-private histograms (p: double, z: uint32) in shared memory
+// small m, MUL: warp-private histograms (p: double, z: uint32) in shared
+// memory, no atomics: in each round every pending lane writes its lane id into
+// the warp's owner slot of its bin; the lane whose id survives updates the bin
+// (plain load/multiply/store), the others retry (rounds = max multiplicity).
 template <class T, class I>
 __global__ void __launch_bounds__(kBThreads) rbi_fwd_smem_mul(const I *__restrict__ inds, const T *__restrict__ as,
                                                               T *__restrict__ ab, RbiParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double *hp = reinterpret_cast<double *>(smem);                              // [nw][m]
-    uint32_t *hz = reinterpret_cast<uint32_t *>(smem + sizeof(double) * nw * P.m);  // [nw][m]
+    double *hp = reinterpret_cast<double *>(smem);                                     // [nw][m]
+    uint32_t *hz = reinterpret_cast<uint32_t *>(smem + sizeof(double) * nw * P.m);     // [nw][m]
+    uint8_t *own = reinterpret_cast<uint8_t *>(hz + (size_t)nw * P.m);                 // [nw][m]
     for (int64_t k = threadIdx.x; k < (int64_t)nw * P.m; k += blockDim.x) { hp[k] = 1.0; hz[k] = 0u; }
     __syncthreads();
     double *wp = hp + warp * P.m;
     uint32_t *wz = hz + warp * P.m;
+    volatile uint8_t *wo = own + warp * P.m;
     rbi_stream<T, I>(inds, as, ab, P, [&](int64_t b, double x, int64_t, bool ok) {
-        // one round per multiplicity: the lowest pending lane of each bin updates it
         bool pending = ok;
         while (__any_sync(0xffffffffu, pending)) {
-            const unsigned key = pending ? (unsigned)b : (0x80000000u | (unsigned)lane);
-            const unsigned same = __match_any_sync(0xffffffffu, key);
-            if (pending && (__ffs(same) - 1) == lane) {
+            if (pending) wo[b] = (uint8_t)lane;
+            __syncwarp();
+            if (pending && wo[b] == (uint8_t)lane) {
                 if (x == 0.0) wz[b] += 1u;
                 else wp[b] *= x;
                 pending = false;
             }
+            __syncwarp();
         }
     });
     __syncthreads();
@@ -248,7 +328,7 @@ __global__ void __launch_bounds__(kBThreads) rbi_add_hist(const I *__restrict__ 
 
 // ------------------------------------------------------------ return
 template <class T>
-struct MulPack {
+struct alignas(16) MulPack {
     double q;   // hs_bar_b * p_b
     int64_t z;  // zero count
 };
@@ -267,48 +347,72 @@ __global__ void rbi_mul_prep(const T *__restrict__ hs_bar, const double *__restr
     }
 }
 
-// ADD (gather) and MUL (three cases) return map
+// ADD (gather) and MUL (three cases) return map; lane-contiguous 4-element
+// groups, two slabs per iteration for 8 independent gathers in flight per lane
 template <class T, class I, int OP>
 __global__ void __launch_bounds__(kBThreads) rbi_bwd_map(const I *__restrict__ inds, const T *__restrict__ as,
                                                          const T *__restrict__ hs_bar, const MulPack<T> *__restrict__ pk,
-                                                         T *__restrict__ ab, int64_t n, int64_t m, int acc) {
-    using IV = IdxVec<I>;
-    auto one = [&](int64_t b, int64_t e) {
-        double v = 0.0;
-        bool touch = true;
-        if (b >= 0 && b < m) {
-            if (OP == VJP_ADD) {
-                v = (double)__ldg(hs_bar + b);
-            } else {
-                const MulPack<T> k = pk[b];
-                if (k.z == 0) {
-                    v = k.q / (double)as[e];  // hs_bar_b * y_b / a_i
-                } else {
-                    const bool zero = (double)as[e] == 0.0;
-                    v = (k.z == 1 && zero) ? k.q : 0.0;  // P:1048-1053 per bin
-                    touch = (k.z == 1 && zero);
-                }
-            }
-        } else {
-            touch = false;
+                                                         T *__restrict__ ab, int64_t n, int64_t m, int acc, int v256) {
+    const uint64_t pol = policy_evict_first();
+    auto val = [&](int64_t b, double a, bool &touch) -> double {
+        touch = false;
+        if (b < 0 || b >= m) return 0.0;
+        if (OP == VJP_ADD) {
+            touch = true;
+            return (double)__ldg(hs_bar + b);
         }
-        if (acc) {
-            if (touch) ab[e] = (T)((double)ab[e] + v);
-        } else {
-            ab[e] = (T)v;
+        const double2 k = __ldg(reinterpret_cast<const double2 *>(pk + b));
+        const int64_t z = (int64_t)__double_as_longlong(k.y);
+        if (z == 0) {
+            touch = true;
+            return k.x / a;  // hs_bar_b * y_b / a_i
         }
+        touch = (z == 1 && a == 0.0);  // P:1048-1053 per bin
+        return touch ? k.x : 0.0;
     };
-    const int64_t nv = n / IV::N;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const typename IV::V *iv = reinterpret_cast<const typename IV::V *>(inds);
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nv; j += stride) {
-        int64_t b[IV::N];
-        IV::get(__ldcs(iv + j), b);
-#pragma unroll
-        for (int q = 0; q < IV::N; ++q) one(b[q], j * IV::N + q);
+    const int lane = threadIdx.x & 31;
+    const int64_t ns = n / 128;
+    const int64_t wstride = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int64_t b[4], bn[4];
+    double a[4] = {0, 0, 0, 0}, an[4] = {0, 0, 0, 0};
+    if (sl < ns) {
+        ld_bins4(inds, sl * 128 + lane * 4, b, pol);
+        if (OP != VJP_ADD) ld_vals4(as, sl * 128 + lane * 4, a, pol, v256);
     }
-    if (blockIdx.x == 0)
-        for (int64_t e = nv * IV::N + threadIdx.x; e < n; e += blockDim.x) one((int64_t)inds[e], e);
+    for (; sl < ns; sl += wstride) {
+        const int64_t e = sl * 128 + lane * 4;
+        const int64_t sn = sl + wstride;
+        if (sn < ns) {  // next slab's loads in flight during this slab's gathers
+            ld_bins4(inds, sn * 128 + lane * 4, bn, pol);
+            if (OP != VJP_ADD) ld_vals4(as, sn * 128 + lane * 4, an, pol, v256);
+        }
+        double o[4] = {0, 0, 0, 0}, r[4];
+        if (acc) ld_acc4(ab, e, o);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            bool touch;
+            const double v = val(b[q], a[q], touch);
+            r[q] = acc ? (touch ? o[q] + v : o[q]) : v;
+        }
+        st_vals4(ab, e, r, pol, v256);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            b[q] = bn[q];
+            a[q] = an[q];
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 32) {
+        for (int64_t e = ns * 128 + lane; e < n; e += 32) {
+            bool touch;
+            const double v = val((int64_t)inds[e], OP == VJP_ADD ? 0.0 : (double)as[e], touch);
+            if (acc) {
+                if (touch) ab[e] = (T)((double)ab[e] + v);
+            } else {
+                ab[e] = (T)v;
+            }
+        }
+    }
 }
 
 // MIN/MAX return: scatter hs_bar[b] to the winner of every bin (as_bar was
@@ -404,6 +508,15 @@ int grid_for(int64_t work, int per_sm) {
     if (g > cap) g = cap;
     return (int)(g < 1 ? 1 : g);
 }
+// persistent grid: exactly the CTAs that fit at once (one wave, no tail)
+template <class K>
+int grid_resident(K kernel, int64_t work, size_t smem = 0) {
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kBThreads, smem) != cudaSuccess || occ < 1) occ = 1;
+    return grid_for(work, occ);
+}
+
+bool a32(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 0; }
 
 RbiParams params(int64_t n, int64_t m, int64_t goff, void *ws, unsigned flags, int zero_fill) {
     BLayout L = blayout(m);
@@ -417,6 +530,7 @@ RbiParams params(int64_t n, int64_t m, int64_t goff, void *ws, unsigned flags, i
     P.p = reinterpret_cast<double *>(w + L.p);
     P.z = reinterpret_cast<unsigned long long *>(w + L.z);
     P.win = reinterpret_cast<Win *>(w + L.win);
+    P.v256 = 0;
     return P;
 }
 
@@ -428,7 +542,7 @@ vjp_status forward(const I *inds, const T *as, T *ab, const RbiParams &P, cudaSt
     const int nvec = (int)(16 / sizeof(I));
     const int64_t work = P.n / nvec + 1;
     if (OP == VJP_MUL) {
-        const size_t sm = (size_t)(kBThreads / 32) * (size_t)P.m * (sizeof(double) + sizeof(uint32_t));
+        const size_t sm = (size_t)(kBThreads / 32) * (size_t)P.m * (sizeof(double) + sizeof(uint32_t) + 1);
         if (sm <= kSmemCap) {
             auto k = rbi_fwd_smem_mul<T, I>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -436,7 +550,7 @@ vjp_status forward(const I *inds, const T *as, T *ab, const RbiParams &P, cudaSt
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kBThreads, sm);
             k<<<grid_for(work, occ < 1 ? 1 : occ), kBThreads, sm, s>>>(inds, as, ab, P);
         } else {
-            rbi_fwd_global<T, I, OP><<<grid_for(work, 8), kBThreads, 0, s>>>(inds, as, ab, P);
+            rbi_fwd_global<T, I, OP><<<grid_resident(rbi_fwd_global<T, I, OP>, work), kBThreads, 0, s>>>(inds, as, ab, P);
         }
     } else {
         const size_t sm = sizeof(Win) * (size_t)P.m;
@@ -447,7 +561,7 @@ vjp_status forward(const I *inds, const T *as, T *ab, const RbiParams &P, cudaSt
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kBThreads, sm);
             k<<<grid_for(work, occ < 1 ? 1 : occ), kBThreads, sm, s>>>(inds, as, ab, P);
         } else {
-            rbi_fwd_global<T, I, OP><<<grid_for(work, 8), kBThreads, 0, s>>>(inds, as, ab, P);
+            rbi_fwd_global<T, I, OP><<<grid_resident(rbi_fwd_global<T, I, OP>, work), kBThreads, 0, s>>>(inds, as, ab, P);
         }
     }
     vjph::count_launch();
@@ -469,16 +583,21 @@ vjp_status run_full(vjp_op op, int64_t n, int64_t m, const void *inds_, const vo
             // primal histogram only on request: atomic adds (order-dependent rounding)
             if (cudaMemsetAsync(hs, 0, sizeof(T) * (size_t)m, s) != cudaSuccess) return VJP_ECUDA;
             RbiParams P = params(n, m, 0, ws, 0, 0);
+            P.v256 = a32(as);
             rbi_add_hist<T, I><<<grid_for(n / nvec + 1, 8), kBThreads, 0, s>>>(inds, as, hs, P);
             vjph::count_launch();
         }
-        rbi_bwd_map<T, I, VJP_ADD><<<grid_for(n / nvec + 1, 8), kBThreads, 0, s>>>(inds, as, hsb, nullptr, ab, n, m, acc);
+        rbi_bwd_map<T, I, VJP_ADD><<<grid_resident(rbi_bwd_map<T, I, VJP_ADD>, n / 4 + 1), kBThreads, 0, s>>>(inds, as, hsb, nullptr, ab, n, m, acc, (int)((!as || a32(as)) && a32(ab)));
         vjph::count_launch();
         if (cudaGetLastError() != cudaSuccess) return VJP_ECUDA;
         if (winners && cudaMemsetAsync(winners, 0xff, sizeof(int64_t) * (size_t)m, s) != cudaSuccess) return VJP_ECUDA;
         return VJP_OK;
     }
-    RbiParams P = params(n, m, 0, ws, flags, (op != VJP_MUL && !acc) ? 1 : 0);
+    // dense MIN/MAX: as_bar = 0 except the winners (a plain memset; the
+    // scatter below overwrites the m winners)
+    if (op != VJP_MUL && !acc && cudaMemsetAsync(ab, 0, sizeof(T) * (size_t)n, s) != cudaSuccess) return VJP_ECUDA;
+    RbiParams P = params(n, m, 0, ws, flags, 0);
+    P.v256 = a32(as) && a32(ab);
     vjp_status st = VJP_OK;
     if (op == VJP_MUL) st = forward<T, I, VJP_MUL>(inds, as, ab, P, s);
     if (op == VJP_MIN) st = forward<T, I, VJP_MIN>(inds, as, ab, P, s);
@@ -488,7 +607,7 @@ vjp_status run_full(vjp_op op, int64_t n, int64_t m, const void *inds_, const vo
     if (op == VJP_MUL) {
         MulPack<T> *pk = reinterpret_cast<MulPack<T> *>(static_cast<unsigned char *>(ws) + L.pk);
         rbi_mul_prep<T><<<grid_for(m, 4), kBThreads, 0, s>>>(hsb, P.p, P.z, pk, m, hs, winners);
-        rbi_bwd_map<T, I, VJP_MUL><<<grid_for(n / nvec + 1, 8), kBThreads, 0, s>>>(inds, as, hsb, pk, ab, n, m, acc);
+        rbi_bwd_map<T, I, VJP_MUL><<<grid_resident(rbi_bwd_map<T, I, VJP_MUL>, n / 4 + 1), kBThreads, 0, s>>>(inds, as, hsb, pk, ab, n, m, acc, (int)(a32(as) && a32(ab)));
         vjph::count_launch(2);
     } else if (op == VJP_MIN) {
         rbi_ext_scatter<T, VJP_MIN><<<grid_for(m, 4), kBThreads, 0, s>>>(P.win, hsb, ab, m, 0, n, acc, hs, winners);
@@ -504,6 +623,7 @@ template <class T, class I>
 vjp_status run_partial(vjp_op op, int64_t n, int64_t m, int64_t goff, const void *inds, const void *as, void *ws,
                        double *bin_val, int64_t *bin_aux, cudaStream_t s) {
     RbiParams P = params(n, m, goff, ws, 0, 0);
+    P.v256 = a32(as);
     vjp_status st = VJP_OK;
     const I *ix = static_cast<const I *>(inds);
     const T *a = static_cast<const T *>(as);
@@ -529,13 +649,13 @@ vjp_status run_finish(vjp_op op, int64_t n, int64_t m, int64_t goff, const void 
     const int acc = (flags & VJP_ACCUMULATE) ? 1 : 0;
     const int nvec = (int)(16 / sizeof(I));
     if (op == VJP_ADD) {
-        rbi_bwd_map<T, I, VJP_ADD><<<grid_for(n / nvec + 1, 8), kBThreads, 0, s>>>(inds, as, hsb, nullptr, ab, n, m, acc);
+        rbi_bwd_map<T, I, VJP_ADD><<<grid_resident(rbi_bwd_map<T, I, VJP_ADD>, n / 4 + 1), kBThreads, 0, s>>>(inds, as, hsb, nullptr, ab, n, m, acc, (int)((!as || a32(as)) && a32(ab)));
     } else if (op == VJP_MUL) {
         BLayout L = blayout(m);
         MulPack<T> *pk = reinterpret_cast<MulPack<T> *>(static_cast<unsigned char *>(ws) + L.pk);
         rbi_mul_prep_ext<T><<<grid_for(m, 4), kBThreads, 0, s>>>(hsb, bin_val, bin_aux, pk, m);
         vjph::count_launch();
-        rbi_bwd_map<T, I, VJP_MUL><<<grid_for(n / nvec + 1, 8), kBThreads, 0, s>>>(inds, as, hsb, pk, ab, n, m, acc);
+        rbi_bwd_map<T, I, VJP_MUL><<<grid_resident(rbi_bwd_map<T, I, VJP_MUL>, n / 4 + 1), kBThreads, 0, s>>>(inds, as, hsb, pk, ab, n, m, acc, (int)(a32(as) && a32(ab)));
     } else {
         rbi_ext_gather<T, I><<<grid_for(n, 8), kBThreads, 0, s>>>(inds, hsb, bin_aux, ab, n, m, goff, acc);
     }

@@ -1,0 +1,127 @@
+"""Multi-process (world_size 2, gloo, CPU) checks of the host-side logic of
+the multi-GPU path: contiguous shard bounds, the rank-ordered all_gather of
+per-shard scan records feeding the carry combination (vjp_scan_carries_host,
+the same __host__ __device__ code the finish kernel runs), and the
+reduce_by_index max/min winner protocol (all_reduce MAX of values, candidate
+selection, all_reduce MIN of global indices) — each against the oracle on the
+unsharded array."""
+from __future__ import annotations
+
+import ctypes
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _mat2_record(A, Y):
+    """[fwd product | D | C] of a shard, from the definitions (P:1137 and the
+    per-element grouping H_i = (ybar_i + H_{i+1}) A_i^T of P:1180)."""
+    P = np.eye(2)
+    for a in A:
+        P = P @ a
+    D, C = np.zeros((2, 2)), np.eye(2)
+    for a, y in zip(A[::-1], Y[::-1]):
+        D = (y + D) @ a.T
+        C = C @ a.T
+    return np.concatenate([P.ravel(), D.ravel(), C.ravel()])
+
+
+def _worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    try:
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+        import oracle
+        import synth
+        import paper_2202_10297_b200 as vjp
+        from paper_2202_10297_b200.dist import shard_bounds
+
+        L = vjp.lib()
+        # ---- scan MAT2: records -> all_gather -> carries -----------------
+        N = 37
+        a, y = synth.mat2_inputs(N)
+        A, Y = a.numpy().reshape(N, 2, 2), y.numpy().reshape(N, 2, 2)
+        off, n = shard_bounds(N, world, rank)
+        rec = torch.from_numpy(_mat2_record(A[off:off + n], Y[off:off + n]))
+        bufs = [torch.empty_like(rec) for _ in range(world)]
+        dist.all_gather(bufs, rec)
+        gathered = torch.cat(bufs).contiguous().numpy()
+        fwd, rev = np.zeros(4), np.zeros(4)
+        rc = L.vjp_scan_carries_host(6, 2, rank, world, gathered.ctypes.data_as(ctypes.c_void_p),
+                                     fwd.ctypes.data_as(ctypes.c_void_p), rev.ctypes.data_as(ctypes.c_void_p))
+        assert rc == 0
+        _, ys = oracle.vjp_scan("mat2", y.numpy(), a.numpy(), want_ys=True)
+        exp_fwd = ys.reshape(N, 4)[off - 1] if off > 0 else np.eye(2).ravel()
+        np.testing.assert_allclose(fwd, exp_fwd, rtol=1e-13)
+        H = np.zeros((2, 2))
+        for j in range(N - 1, off + n - 1, -1):
+            H = (Y[j] + H) @ A[j].T
+        np.testing.assert_allclose(rev, H.ravel(), rtol=1e-12, atol=1e-300)
+
+        # ---- reduce_by_index MAX winners: the 3-step collective protocol ----
+        M, NN = 50, 2000
+        inds, av, hb = synth.rbi_inputs(NN, M, "max")
+        off, n = shard_bounds(NN, world, rank)
+        _, hs_loc, win_loc, _ = oracle.vjp_reduce_by_index("max", inds.numpy()[off:off + n], av.numpy()[off:off + n],
+                                                          hb.numpy())
+        val = torch.from_numpy(np.where(win_loc >= 0, hs_loc, -np.inf))
+        aux = torch.from_numpy(np.where(win_loc >= 0, win_loc + off, np.iinfo(np.int64).max))
+        gval = val.clone()
+        dist.all_reduce(gval, op=dist.ReduceOp.MAX)
+        aux = torch.where(val == gval, aux, torch.full_like(aux, np.iinfo(np.int64).max))
+        dist.all_reduce(aux, op=dist.ReduceOp.MIN)
+        _, _, win_full, _ = oracle.vjp_reduce_by_index("max", inds.numpy(), av.numpy(), hb.numpy())
+        got = aux.numpy().copy()
+        got[got == np.iinfo(np.int64).max] = -1
+        assert np.array_equal(got, win_full)
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put((rank, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("world", [2])
+def test_dist_protocols_gloo(world):
+    from paper_2202_10297_b200 import _build
+    _build.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    for r in range(world):
+        assert res[r] == "ok", res[r]
+
+
+def test_shard_bounds_cover():
+    from paper_2202_10297_b200.dist import shard_bounds
+    for N in (0, 1, 7, 1000, 10**6 + 3):
+        for W in (1, 2, 3, 8):
+            bs = [shard_bounds(N, W, r) for r in range(W)]
+            assert bs[0][0] == 0
+            for (o1, n1), (o2, _) in zip(bs, bs[1:]):
+                assert o1 + n1 == o2
+            assert sum(n for _, n in bs) == N
+            assert max(n for _, n in bs) - min(n for _, n in bs) <= 1
