@@ -252,7 +252,7 @@ def run_ours(args):
         prof = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(prof):
             try:
-                traffic = json.load(open(prof)).get("scan_pass2_mat2_f64_n2^26")
+                traffic = json.load(open(prof)).get("scan_apply_mat2_f64_n2^26") if n == (1 << 26) else None
             except Exception:
                 traffic = None
         cpu = None
@@ -270,11 +270,11 @@ def run_ours(args):
                        "l2": "no flush: every array >= 1 GiB >> 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "scan_pass2<OpMat2,f64> (MAT2 return sweep)",
+                         "kernel": "scan_apply<OpMat2,f64> (MAT2 return sweep, chunked)",
                          "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": kmat2,
                          "peak_source": peak_src,
-                         "linrec_pass2_ms": statistics.mean(k_lin),
-                         "linrec_pass2_gbs": 48 * n / (statistics.mean(k_lin) * 1e-3) / 1e9,
+                         "linrec_apply_ms": statistics.mean(k_lin),
+                         "linrec_apply_gbs": 48 * n / (statistics.mean(k_lin) * 1e-3) / 1e9,
                          "step_alg_gbs": (64 + 128) * n / (mean_ms * 1e-3) / 1e9},
             "cpu_baseline": cpu,
             "e2e": e2e,
