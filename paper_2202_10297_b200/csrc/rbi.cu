@@ -65,38 +65,6 @@ __device__ __forceinline__ bool win_better(uint64_t k, uint64_t i, uint64_t ck, 
     return k > ck || (k == ck && i > ci);
 }
 
-__device__ __forceinline__ void cas128_global(Win *w, uint64_t k, uint64_t i) {
-    uint64_t ck = __ldcg(reinterpret_cast<const unsigned long long *>(&w->key));
-    if (k < ck) return;  // monotone filter: the stored key never decreases
-    uint64_t ci = __ldcg(reinterpret_cast<const unsigned long long *>(&w->inv));
-    while (win_better(k, i, ck, ci)) {
-        uint64_t ok, oi;
-        asm volatile(
-            "{ .reg .b128 c, s, r; mov.b128 c, {%2,%3}; mov.b128 s, {%4,%5};"
-            " atom.global.cas.b128 r, [%6], c, s; mov.b128 {%0,%1}, r; }"
-            : "=l"(ok), "=l"(oi) : "l"(ck), "l"(ci), "l"(k), "l"(i), "l"(w) : "memory");
-        if (ok == ck && oi == ci) return;
-        ck = ok;
-        ci = oi;
-    }
-}
-__device__ __forceinline__ void cas128_shared(Win *w, uint64_t k, uint64_t i) {
-    uint64_t ck = *reinterpret_cast<volatile uint64_t *>(&w->key);
-    if (k < ck) return;
-    uint64_t ci = *reinterpret_cast<volatile uint64_t *>(&w->inv);
-    const uint32_t a = smem_u32(w);
-    while (win_better(k, i, ck, ci)) {
-        uint64_t ok, oi;
-        asm volatile(
-            "{ .reg .b128 c, s, r; mov.b128 c, {%2,%3}; mov.b128 s, {%4,%5};"
-            " atom.shared.cas.b128 r, [%6], c, s; mov.b128 {%0,%1}, r; }"
-            : "=l"(ok), "=l"(oi) : "l"(ck), "l"(ci), "l"(k), "l"(i), "r"(a) : "memory");
-        if (ok == ck && oi == ci) return;
-        ck = ok;
-        ci = oi;
-    }
-}
-
 __device__ __forceinline__ void mul_cas_global(double *addr, double x) {
     unsigned long long *a = reinterpret_cast<unsigned long long *>(addr);
     unsigned long long old = __ldcg(a), assumed;
@@ -112,14 +80,24 @@ struct RbiParams {
     int32_t v256, pad;  // value arrays 32-byte aligned: 256-bit accesses
     double *p;        // MUL: [m] product of nonzeros
     unsigned long long *z;  // MUL: [m] zero count
-    Win *win;         // MIN/MAX: [m]
+    Win *win;         // MIN/MAX: [m] {value key (max), ~index (max)}
+    unsigned long long *ng;     // MUL, log domain: [m] count of negative factors
+    int32_t log_domain, pad2;   // MUL, large m: p holds sum log2|a| until finalised
+    unsigned long long *cand;   // MIN/MAX: candidate list [cap][3] = {key, global index, bin}
+    unsigned long long *ncand;  // candidate counter
+    int64_t cap;
 };
 
 // ------------------------------------------------------------ init
 template <int OP>
 __global__ void rbi_init(RbiParams P) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && P.ncand) *P.ncand = 0ull;
     for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < P.m; b += (int64_t)gridDim.x * blockDim.x) {
-        if (OP == VJP_MUL) { P.p[b] = 1.0; P.z[b] = 0ull; }
+        if (OP == VJP_MUL) {
+            P.p[b] = P.log_domain ? 0.0 : 1.0;
+            P.z[b] = 0ull;
+            if (P.log_domain) P.ng[b] = 0ull;
+        }
         else { P.win[b].key = 0ull; P.win[b].inv = 0ull; }
     }
 }
@@ -241,37 +219,137 @@ __device__ __forceinline__ void rbi_stream(const I *__restrict__ inds, const T *
     }
 }
 
-// large m: global atomics
+// MUL, large m: global CAS multiply + atomicAdd of the zero count
 template <class T, class I, int OP>
 __global__ void __launch_bounds__(kBThreads) rbi_fwd_global(const I *__restrict__ inds, const T *__restrict__ as,
                                                             T *__restrict__ ab, RbiParams P) {
-    const bool is_min = OP == VJP_MIN;
-    rbi_stream<T, I>(inds, as, ab, P, [&](int64_t b, double x, int64_t gi, bool ok) {
+    rbi_stream<T, I>(inds, as, ab, P, [&](int64_t b, double x, int64_t, bool ok) {
         if (!ok) return;
-        if (OP == VJP_MUL) {
-            if (x == 0.0) atomicAdd(P.z + b, 1ull);
-            else mul_cas_global(P.p + b, x);
-        } else {
-            cas128_global(P.win + b, ord_key(x, is_min), ~(uint64_t)gi);
-        }
+        if (x == 0.0) atomicAdd(P.z + b, 1ull);
+        else mul_cas_global(P.p + b, x);
     });
 }
 
-// small m, MIN/MAX: one shared-memory Win[m] per CTA, filtered CAS, then merged
-template <class T, class I, int OP>
-__global__ void __launch_bounds__(kBThreads) rbi_fwd_smem_ext(const I *__restrict__ inds, const T *__restrict__ as,
-                                                              T *__restrict__ ab, RbiParams P) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    Win *h = reinterpret_cast<Win *>(smem);
-    const bool is_min = OP == VJP_MIN;
-    for (int64_t b = threadIdx.x; b < P.m; b += blockDim.x) { h[b].key = 0ull; h[b].inv = 0ull; }
-    __syncthreads();
-    rbi_stream<T, I>(inds, as, ab, P, [&](int64_t b, double x, int64_t gi, bool ok) {
-        if (ok) cas128_shared(h + b, ord_key(x, is_min), ~(uint64_t)gi);
+// MUL, large m: every element must contribute, and a CAS-multiply costs two
+// dependent L2 round trips per element.  Instead accumulate log2|a| with
+// fire-and-forget f64 red.add, count zeros and negative factors, and finalise
+// p_b = (-1)^neg * exp2(sum) per bin.  Error: <= 1 ulp per log2 plus the
+// summation order, i.e. ~ n_b * u * max|log2 a| relative (~3e-13 for
+// |log2 a| ~ 10 and n_b = 268) — inside the 1e-10 tolerance; the domain
+// assumption R13 (p finite and normal) is unchanged.
+template <class T, class I>
+__global__ void __launch_bounds__(kBThreads) rbi_fwd_log(const I *__restrict__ inds, const T *__restrict__ as,
+                                                         RbiParams P) {
+    rbi_stream<T, I>(inds, as, nullptr, P, [&](int64_t b, double x, int64_t, bool ok) {
+        if (!ok) return;
+        if (x == 0.0) {
+            atomicAdd(P.z + b, 1ull);
+        } else {
+            atomicAdd(P.p + b, log2(fabs(x)));
+            if (x < 0.0) atomicAdd(P.ng + b, 1ull);
+        }
     });
-    __syncthreads();
-    for (int64_t b = threadIdx.x; b < P.m; b += blockDim.x)
-        if (h[b].key) cas128_global(P.win + b, h[b].key, h[b].inv);
+}
+__global__ void rbi_log_finalize(RbiParams P) {
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < P.m; b += (int64_t)gridDim.x * blockDim.x) {
+        const double v = exp2(P.p[b]);
+        P.p[b] = (P.ng[b] & 1ull) ? -v : v;
+    }
+}
+
+__device__ __forceinline__ void red_max_u64(unsigned long long *a, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.max.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void red_max_u64_shared(unsigned long long *a, unsigned long long v) {
+    asm volatile("red.relaxed.cta.shared::cta.max.u64 [%0], %1;" ::"r"(smem_u32(a)), "l"(v) : "memory");
+}
+
+// MIN/MAX phase A: per-bin extremum of the value key.  The stored key only
+// grows, so an element whose key is below a stored key can never win: skip
+// it; otherwise fire-and-forget red.max (no round trip, no divergent wait)
+// and append it to the warp's own region of the candidate list (no shared
+// counter).  Every eventual winner passes the filter (its key >= any stored
+// key).  SMEM (small m): the filter is a per-CTA shared-memory table merged
+// into the global keys at the end; large m: the global keys in L2.
+template <class T, class I, int OP, bool SMEM>
+__global__ void __launch_bounds__(kBThreads) rbi_ext_a(const I *__restrict__ inds, const T *__restrict__ as,
+                                                       RbiParams P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    unsigned long long *hk = reinterpret_cast<unsigned long long *>(smem);
+    const bool is_min = OP == VJP_MIN;
+    const int lane = threadIdx.x & 31;
+    if (SMEM) {
+        for (int64_t b = threadIdx.x; b < P.m; b += blockDim.x) hk[b] = 0ull;
+        __syncthreads();
+    }
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t R = P.cap / nw;  // this warp's region of the candidate list
+    unsigned long long *reg = P.cand + 3 * gw * R;
+    int64_t cnt = 0;
+    rbi_stream<T, I>(inds, as, nullptr, P, [&](int64_t b, double x, int64_t gi, bool ok) {
+        uint64_t k = 0;
+        bool cand = false;
+        if (ok) {
+            k = ord_key(x, is_min);
+            unsigned long long *slot = SMEM ? hk + b : reinterpret_cast<unsigned long long *>(&P.win[b].key);
+            const uint64_t ck = SMEM ? *reinterpret_cast<volatile unsigned long long *>(slot) : __ldcg(slot);
+            cand = k >= ck;
+            if (k > ck) {
+                if (SMEM) red_max_u64_shared(slot, k);
+                else red_max_u64(slot, k);
+            }
+        }
+        const unsigned msk = __ballot_sync(0xffffffffu, cand);
+        if (cand) {
+            const int64_t q = cnt + __popc(msk & ((1u << lane) - 1u));
+            if (q < R) {
+                unsigned long long *c = reg + 3 * q;
+                c[0] = k;
+                c[1] = (unsigned long long)gi;
+                c[2] = (unsigned long long)b;
+            }
+        }
+        cnt += __popc(msk);
+    });
+    if (lane == 0) {
+        P.ncand[1 + gw] = (unsigned long long)cnt;
+        if (cnt > R) atomicOr(P.ncand, 1ull);  // overflow: phase B re-reads the inputs
+    }
+    if (SMEM) {
+        __syncthreads();
+        for (int64_t b = threadIdx.x; b < P.m; b += blockDim.x)
+            if (hk[b]) red_max_u64(reinterpret_cast<unsigned long long *>(&P.win[b].key), hk[b]);
+    }
+}
+
+// MIN/MAX phase B: among the elements whose key equals the final per-bin key,
+// the LOWEST global index wins (red.max of ~index).  Walks the candidate list,
+// or (if it overflowed) re-reads the inputs.
+template <class T, class I, int OP>
+__global__ void __launch_bounds__(kBThreads) rbi_ext_b(const I *__restrict__ inds, const T *__restrict__ as,
+                                                       RbiParams P, int64_t nwa) {
+    const bool is_min = OP == VJP_MIN;
+    if (__ldcg(P.ncand) == 0ull) {
+        // walk every phase-A warp's region (nwa warps, R entries each)
+        const int64_t R = P.cap / nwa;
+        const int64_t total = nwa * R;
+        for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < total;
+             c += (int64_t)gridDim.x * blockDim.x) {
+            const int64_t w = c / R, q = c - w * R;
+            if (q >= (int64_t)__ldcg(P.ncand + 1 + w)) continue;
+            const unsigned long long *e = P.cand + 3 * c;
+            const int64_t b = (int64_t)e[2];
+            if (e[0] == __ldcg(reinterpret_cast<const unsigned long long *>(&P.win[b].key)))
+                red_max_u64(reinterpret_cast<unsigned long long *>(&P.win[b].inv), ~e[1]);
+        }
+        return;
+    }
+    rbi_stream<T, I>(inds, as, nullptr, P, [&](int64_t b, double x, int64_t gi, bool ok) {
+        if (ok && ord_key(x, is_min) == __ldcg(reinterpret_cast<const unsigned long long *>(&P.win[b].key)))
+            red_max_u64(reinterpret_cast<unsigned long long *>(&P.win[b].inv), ~(uint64_t)gi);
+    });
 }
 
 // small m, MUL: warp-private histograms (p: double, z: uint32) in shared
@@ -485,19 +563,33 @@ namespace {
 using namespace vjpk;
 
 constexpr size_t kSmemCap = 200 * 1024;
+constexpr int64_t kMaxWarpsA = 65536;  // phase-A warps (per-warp candidate counts)
 
 bool op_ok(vjp_op op) { return op == VJP_ADD || op == VJP_MUL || op == VJP_MIN || op == VJP_MAX; }
 
 struct BLayout {
-    size_t p, z, win, pk, total;
+    size_t p, z, ng, win, pk, ncand, cand, total;
+    int64_t cap;
 };
-BLayout blayout(int64_t m) {
+// candidate list capacity for MIN/MAX: ~(H(n/m) + ties) per bin are expected;
+// overflow is handled (phase B re-reads the inputs)
+int64_t cand_cap(int64_t n, int64_t m) {
+    int64_t c = n / 16;
+    if (c < 16 * m) c = 16 * m;
+    if (c < (1 << 16)) c = 1 << 16;
+    return c;
+}
+BLayout blayout(int64_t m, int64_t n = 0, bool ext = false) {
     BLayout L{};
     size_t off = 0;
     L.p = off; off += vjph::align256(sizeof(double) * (size_t)m);
     L.z = off; off += vjph::align256(sizeof(unsigned long long) * (size_t)m);
+    L.ng = off; off += vjph::align256(sizeof(unsigned long long) * (size_t)m);
     L.win = off; off += vjph::align256(sizeof(Win) * (size_t)m);
     L.pk = off; off += vjph::align256(16 * (size_t)m);
+    L.ncand = off; off += vjph::align256(8 * (1 + kMaxWarpsA));
+    L.cap = ext ? cand_cap(n, m) : 0;
+    L.cand = off; off += vjph::align256((size_t)L.cap * 24);
     L.total = off;
     return L;
 }
@@ -518,8 +610,8 @@ int grid_resident(K kernel, int64_t work, size_t smem = 0) {
 
 bool a32(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 0; }
 
-RbiParams params(int64_t n, int64_t m, int64_t goff, void *ws, unsigned flags, int zero_fill) {
-    BLayout L = blayout(m);
+RbiParams params(int64_t n, int64_t m, int64_t goff, void *ws, unsigned flags, int zero_fill, bool ext = false) {
+    BLayout L = blayout(m, n, ext);
     unsigned char *w = static_cast<unsigned char *>(ws);
     RbiParams P{};
     P.n = n;
@@ -530,39 +622,54 @@ RbiParams params(int64_t n, int64_t m, int64_t goff, void *ws, unsigned flags, i
     P.p = reinterpret_cast<double *>(w + L.p);
     P.z = reinterpret_cast<unsigned long long *>(w + L.z);
     P.win = reinterpret_cast<Win *>(w + L.win);
+    P.ng = reinterpret_cast<unsigned long long *>(w + L.ng);
+    P.ncand = reinterpret_cast<unsigned long long *>(w + L.ncand);
+    P.cand = reinterpret_cast<unsigned long long *>(w + L.cand);
+    P.cap = L.cap;
     P.v256 = 0;
     return P;
 }
 
 // forward histogram (MUL / MIN / MAX), init included
 template <class T, class I, int OP>
-vjp_status forward(const I *inds, const T *as, T *ab, const RbiParams &P, cudaStream_t s) {
+vjp_status forward(const I *inds, const T *as, T *ab, RbiParams P, cudaStream_t s) {
+    const size_t sm_mul = (size_t)(kBThreads / 32) * (size_t)P.m * (sizeof(double) + sizeof(uint32_t) + 1);
+    P.log_domain = (OP == VJP_MUL && sm_mul > kSmemCap) ? 1 : 0;
     rbi_init<OP><<<grid_for(P.m, 4), kBThreads, 0, s>>>(P);
     vjph::count_launch();
     const int nvec = (int)(16 / sizeof(I));
     const int64_t work = P.n / nvec + 1;
     if (OP == VJP_MUL) {
-        const size_t sm = (size_t)(kBThreads / 32) * (size_t)P.m * (sizeof(double) + sizeof(uint32_t) + 1);
-        if (sm <= kSmemCap) {
+        const size_t sm = sm_mul;
+        if (!P.log_domain) {
             auto k = rbi_fwd_smem_mul<T, I>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             int occ = 1;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kBThreads, sm);
             k<<<grid_for(work, occ < 1 ? 1 : occ), kBThreads, sm, s>>>(inds, as, ab, P);
         } else {
-            rbi_fwd_global<T, I, OP><<<grid_resident(rbi_fwd_global<T, I, OP>, work), kBThreads, 0, s>>>(inds, as, ab, P);
+            rbi_fwd_log<T, I><<<grid_resident(rbi_fwd_log<T, I>, work), kBThreads, 0, s>>>(inds, as, P);
+            vjph::count_launch();
+            rbi_log_finalize<<<grid_for(P.m, 4), kBThreads, 0, s>>>(P);
         }
     } else {
-        const size_t sm = sizeof(Win) * (size_t)P.m;
-        if (sm <= kSmemCap && P.m <= 16384) {
-            auto k = rbi_fwd_smem_ext<T, I, OP>;
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            int occ = 1;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kBThreads, sm);
-            k<<<grid_for(work, occ < 1 ? 1 : occ), kBThreads, sm, s>>>(inds, as, ab, P);
+        const size_t smk = sizeof(unsigned long long) * (size_t)P.m;
+        int ga;
+        if (smk <= 128 * 1024) {
+            auto k = rbi_ext_a<T, I, OP, true>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smk);
+            ga = grid_resident(k, work, smk);
+            if ((int64_t)ga * (kBThreads / 32) > kMaxWarpsA) ga = (int)(kMaxWarpsA / (kBThreads / 32));
+            k<<<ga, kBThreads, smk, s>>>(inds, as, P);
         } else {
-            rbi_fwd_global<T, I, OP><<<grid_resident(rbi_fwd_global<T, I, OP>, work), kBThreads, 0, s>>>(inds, as, ab, P);
+            auto k = rbi_ext_a<T, I, OP, false>;
+            ga = grid_resident(k, work);
+            if ((int64_t)ga * (kBThreads / 32) > kMaxWarpsA) ga = (int)(kMaxWarpsA / (kBThreads / 32));
+            k<<<ga, kBThreads, 0, s>>>(inds, as, P);
         }
+        vjph::count_launch();
+        rbi_ext_b<T, I, OP><<<grid_resident(rbi_ext_b<T, I, OP>, work), kBThreads, 0, s>>>(inds, as, P,
+                                                                                           (int64_t)ga * (kBThreads / 32));
     }
     vjph::count_launch();
     return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
@@ -596,7 +703,7 @@ vjp_status run_full(vjp_op op, int64_t n, int64_t m, const void *inds_, const vo
     // dense MIN/MAX: as_bar = 0 except the winners (a plain memset; the
     // scatter below overwrites the m winners)
     if (op != VJP_MUL && !acc && cudaMemsetAsync(ab, 0, sizeof(T) * (size_t)n, s) != cudaSuccess) return VJP_ECUDA;
-    RbiParams P = params(n, m, 0, ws, flags, 0);
+    RbiParams P = params(n, m, 0, ws, flags, 0, op != VJP_MUL);
     P.v256 = a32(as) && a32(ab);
     vjp_status st = VJP_OK;
     if (op == VJP_MUL) st = forward<T, I, VJP_MUL>(inds, as, ab, P, s);
@@ -622,7 +729,7 @@ vjp_status run_full(vjp_op op, int64_t n, int64_t m, const void *inds_, const vo
 template <class T, class I>
 vjp_status run_partial(vjp_op op, int64_t n, int64_t m, int64_t goff, const void *inds, const void *as, void *ws,
                        double *bin_val, int64_t *bin_aux, cudaStream_t s) {
-    RbiParams P = params(n, m, goff, ws, 0, 0);
+    RbiParams P = params(n, m, goff, ws, 0, 0, op != VJP_MUL);
     P.v256 = a32(as);
     vjp_status st = VJP_OK;
     const I *ix = static_cast<const I *>(inds);
@@ -651,7 +758,7 @@ vjp_status run_finish(vjp_op op, int64_t n, int64_t m, int64_t goff, const void 
     if (op == VJP_ADD) {
         rbi_bwd_map<T, I, VJP_ADD><<<grid_resident(rbi_bwd_map<T, I, VJP_ADD>, n / 4 + 1), kBThreads, 0, s>>>(inds, as, hsb, nullptr, ab, n, m, acc, (int)((!as || a32(as)) && a32(ab)));
     } else if (op == VJP_MUL) {
-        BLayout L = blayout(m);
+        BLayout L = blayout(m, n, false);
         MulPack<T> *pk = reinterpret_cast<MulPack<T> *>(static_cast<unsigned char *>(ws) + L.pk);
         rbi_mul_prep_ext<T><<<grid_for(m, 4), kBThreads, 0, s>>>(hsb, bin_val, bin_aux, pk, m);
         vjph::count_launch();
@@ -686,9 +793,9 @@ extern "C" {
 size_t vjp_reduce_by_index_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_t n, int64_t m) {
     (void)dtype;
     (void)n;
-    if (!op_ok(op) || m < 1) return 0;
+    if (!op_ok(op) || m < 1 || n < 0) return 0;
     if (op == VJP_ADD) return 0;
-    return blayout(m).total;
+    return blayout(m, n, op != VJP_MUL).total;
 }
 
 vjp_status vjp_reduce_by_index(vjp_op op, vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, const void *inds,
@@ -715,11 +822,11 @@ vjp_status vjp_reduce_by_index_partial(vjp_op op, vjp_dtype dtype, vjp_itype ity
     vjp_status st = common_check(op, dtype, itype, n, m, inds, as, inds);
     if (st != VJP_OK) return st;
     if (!bin_val || !bin_aux) return VJP_EINVAL;
-    if (ws_bytes < blayout(m).total || !ws) return VJP_EWORKSPACE;
+    if (ws_bytes < blayout(m, n, op != VJP_MUL).total || !ws) return VJP_EWORKSPACE;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (n == 0) {
         // empty shard: neutral per-bin state
-        RbiParams P = params(0, m, shard->global_offset, ws, 0, 0);
+        RbiParams P = params(0, m, shard->global_offset, ws, 0, 0, op != VJP_MUL);
         if (op == VJP_MUL) { rbi_init<VJP_MUL><<<grid_for(m, 4), kBThreads, 0, s>>>(P); rbi_export<VJP_MUL><<<grid_for(m, 4), kBThreads, 0, s>>>(P, bin_val, bin_aux); }
         if (op == VJP_MIN) { rbi_init<VJP_MIN><<<grid_for(m, 4), kBThreads, 0, s>>>(P); rbi_export<VJP_MIN><<<grid_for(m, 4), kBThreads, 0, s>>>(P, bin_val, bin_aux); }
         if (op == VJP_MAX) { rbi_init<VJP_MAX><<<grid_for(m, 4), kBThreads, 0, s>>>(P); rbi_export<VJP_MAX><<<grid_for(m, 4), kBThreads, 0, s>>>(P, bin_val, bin_aux); }
