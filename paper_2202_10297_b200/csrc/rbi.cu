@@ -346,7 +346,9 @@ __global__ void __launch_bounds__(kBThreads) rbi_ext_b(const I *__restrict__ ind
         }
         return;
     }
-    rbi_stream<T, I>(inds, as, nullptr, P, [&](int64_t b, double x, int64_t gi, bool ok) {
+    RbiParams Q = P;
+    Q.zero_fill = 0;  // the fallback only re-reads
+    rbi_stream<T, I>(inds, as, nullptr, Q, [&](int64_t b, double x, int64_t gi, bool ok) {
         if (ok && ord_key(x, is_min) == __ldcg(reinterpret_cast<const unsigned long long *>(&P.win[b].key)))
             red_max_u64(reinterpret_cast<unsigned long long *>(&P.win[b].inv), ~(uint64_t)gi);
     });
