@@ -74,11 +74,12 @@ def test_scan_parity_lookback_path(op):
 @pytest.mark.parametrize("dt", [np.float64, np.float32], ids=["f64", "f32"])
 def test_scan_add_integer_seeds_bit_exact(dt):
     """integer seeds in [-8, 8]: every summation order is exact."""
-    for n in (10_000, 1 << 20, (1 << 20) + 3):
+    for n in (10_000, 1 << 20, (1 << 20) + 3, 5_000_011):
         yb = synth.scan_add_seed(n, kind="int", dtype=TD[dt])
         ref = oracle.vjp_scan("add", yb.numpy(), None)
-        got = vjp.scan("add", yb.to(DEV)).cpu().numpy()
-        assert np.array_equal(got, ref)
+        for kw in ({}, {"lookback": True}):
+            got = vjp.scan("add", yb.to(DEV), **kw).cpu().numpy()
+            assert np.array_equal(got, ref), kw
 
 
 def test_scan_add_config1_closed_form():
