@@ -240,6 +240,61 @@ __global__ void __launch_bounds__(kRThreads) reduce_bwd(const T *__restrict__ as
         return p.acc ? old + v : v;
     };
     const bool need_a = (OP == VJP_MUL && st.b == 0);
+    if (!p.acc) {
+        // overwrite mode: 4 independent 16-byte vectors per thread per iteration
+        int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        if (need_a) {  // MUL, no zero: as_bar_i = ybar * p / a_i
+            for (; j + 3 * stride < nv; j += 4 * stride) {
+                typename VV::V v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = __ldcs(av + j + u * stride);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    double a[VV::N], r[VV::N];
+                    VV::get(v[u], a);
+#pragma unroll
+                    for (int q2 = 0; q2 < VV::N; ++q2) r[q2] = q / a[q2];
+                    __stcs(bv + j + u * stride, VV::make(r));
+                }
+            }
+        } else {  // ADD broadcast, or zeros with at most one point value (sparse cases)
+            const int64_t pv = (point != kNoIdx && point >= p.goff && point < p.goff + p.n) ? (point - p.goff) / VV::N : -1;
+            double fill = (OP == VJP_ADD) ? yb : 0.0;
+            double f[VV::N];
+#pragma unroll
+            for (int q2 = 0; q2 < VV::N; ++q2) f[q2] = fill;
+            const typename VV::V fv = VV::make(f);
+            for (; j + 3 * stride < nv; j += 4 * stride) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t jj = j + u * stride;
+                    if (jj == pv) {
+                        double r[VV::N];
+#pragma unroll
+                        for (int q2 = 0; q2 < VV::N; ++q2) r[q2] = value(0.0, p.goff + jj * VV::N + q2, 0.0);
+                        __stcs(bv + jj, VV::make(r));
+                    } else {
+                        __stcs(bv + jj, fv);
+                    }
+                }
+            }
+        }
+        // remainder vectors: generic path below
+        for (; j < nv; j += stride) {
+            double a[VV::N] = {}, r[VV::N];
+            if (need_a) VV::get(__ldcs(av + j), a);
+#pragma unroll
+            for (int q2 = 0; q2 < VV::N; ++q2) r[q2] = value(a[q2], p.goff + j * VV::N + q2, 0.0);
+            __stcs(bv + j, VV::make(r));
+        }
+        if (blockIdx.x == 0) {
+            for (int64_t e = nv * VV::N + threadIdx.x; e < p.n; e += blockDim.x) {
+                double a = need_a ? (double)as[e] : 0.0;
+                ab[e] = (T)value(a, p.goff + e, 0.0);
+            }
+        }
+        return;
+    }
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < nv; j += stride) {
         double a[VV::N] = {}, o[VV::N] = {}, r[VV::N];
         if (need_a) VV::get(__ldcs(av + j), a);
