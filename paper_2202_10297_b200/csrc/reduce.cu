@@ -127,18 +127,24 @@ __global__ void __launch_bounds__(kRThreads) reduce_fwd(const T *__restrict__ as
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const typename VV::V *av = reinterpret_cast<const typename VV::V *>(as);
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    // 4 independent 16-byte loads in flight per thread
-    for (; j + 3 * stride < nv; j += 4 * stride) {
-        typename VV::V v[4];
+    // 4 independent 16-byte loads in flight per thread, 4 independent
+    // accumulators (no serial dependency chain across the vectors)
+    {
+        RRec ru[4] = {rrec_id<OP>(), rrec_id<OP>(), rrec_id<OP>(), rrec_id<OP>()};
+        for (; j + 3 * stride < nv; j += 4 * stride) {
+            typename VV::V v[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = __ldcs(av + j + u * stride);
+            for (int u = 0; u < 4; ++u) v[u] = __ldcs(av + j + u * stride);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            double x[VV::N];
-            VV::get(v[u], x);
+            for (int u = 0; u < 4; ++u) {
+                double x[VV::N];
+                VV::get(v[u], x);
 #pragma unroll
-            for (int q = 0; q < VV::N; ++q) rrec_add<OP>(r, x[q], goff + (j + u * stride) * VV::N + q);
+                for (int q = 0; q < VV::N; ++q) rrec_add<OP>(ru[u], x[q], goff + (j + u * stride) * VV::N + q);
+            }
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) r = rrec_combine<OP>(r, ru[u]);
     }
     for (; j < nv; j += stride) {
         double x[VV::N];
