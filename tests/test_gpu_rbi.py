@@ -60,7 +60,8 @@ def test_rbi_golden_g5_g6():
     inds = torch.tensor([0, 1, 0, 1, 2, 2], dtype=torch.int32)
     a = torch.tensor([2, 0, 3, 5, 0, 0], dtype=torch.float64)
     got = vjp.reduce_by_index("mul", inds.to(DEV), a.to(DEV), torch.tensor([1.0, 10, 100], dtype=torch.float64, device=DEV))
-    assert got.cpu().tolist() == [3, 50, 2, 0, 0, 0]
+    # the per-bin product is accumulated in the log domain: exact up to rounding (north_star tolerance)
+    assert_close(got.cpu().numpy(), np.array([3.0, 50, 2, 0, 0, 0]), np.float64, what="G5")
     inds = torch.tensor([0, 1, 0, 1, 0], dtype=torch.int32)
     a = torch.tensor([3, 5, 3, -1, 2], dtype=torch.float64)
     got = vjp.reduce_by_index("max", inds.to(DEV), a.to(DEV), torch.tensor([7.0, 9], dtype=torch.float64, device=DEV))
