@@ -152,10 +152,15 @@ def run_ours(args):
 
     world, rank, local = dist_env()
     assert world == args.gpus or world == 1, "--gpus must match WORLD_SIZE"
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    ndev = torch.cuda.device_count()
+    torch.cuda.set_device(local % ndev)
+    dev = torch.device("cuda", local % ndev)
+    backend = os.environ.get("VJP_DIST_BACKEND", "nccl")  # gloo: test several ranks on one GPU
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     vjp.lib()
 
     n = args.n or (1 << 26)
@@ -190,7 +195,7 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    with ClockSampler(local % ndev) as clk:
         for i in range(args.steps):
             starts[i].record()
             step(kev[i])
@@ -266,7 +271,8 @@ def run_ours(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (synth/, seed 2202)",
             "config": {"workload": "configs[1]: vjp_scan LINREC + MAT2, n = 2^26 elements per op per GPU, f64",
                        "n_per_op_per_gpu": n, "global_n_per_op": gN, "ops": ops,
-                       "parallelism": f"contiguous shards x{world}, all_gather of shard aggregates",
+                       "parallelism": f"contiguous shards x{world}, all_gather of shard aggregates"
+                                      + ("" if world == 1 else f" ({backend})"),
                        "l2": "no flush: every array >= 1 GiB >> 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,

@@ -24,6 +24,26 @@ import torch.distributed as dist
 from . import (ACCUMULATE, WIDTH, VjpShard, _check, _dt, _it, _op, _p, _stream, lib, workspace)
 
 
+def _all_gather_into(out: torch.Tensor, inp: torch.Tensor, group=None):
+    """all_gather of a small device record; NCCL directly, gloo (CPU testing
+    of the multi-rank path, e.g. several ranks on one GPU) through host memory."""
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, inp, group=group)
+        return
+    parts = [torch.empty_like(inp, device="cpu") for _ in range(dist.get_world_size(group))]
+    dist.all_gather(parts, inp.cpu(), group=group)
+    out.copy_(torch.cat(parts).to(out.device))
+
+
+def _all_reduce(t: torch.Tensor, op, group=None):
+    if dist.get_backend(group) == "nccl":
+        dist.all_reduce(t, op=op, group=group)
+        return
+    h = t.cpu()
+    dist.all_reduce(h, op=op, group=group)
+    t.copy_(h.to(t.device))
+
+
 def shard_bounds(global_n: int, world: int, rank: int) -> tuple[int, int]:
     """contiguous, balanced split; rank r gets [off, off + n)."""
     base, rem = divmod(global_n, world)
@@ -65,7 +85,7 @@ def scan(op, ys_bar: torch.Tensor, as_: torch.Tensor | None, *, offset: int, glo
     gathered = None
     if world > 1:
         gathered = torch.empty(world * rec, dtype=torch.float64, device=dev)
-        dist.all_gather_into_tensor(gathered, part, group=group)
+        _all_gather_into(gathered, part, group)
     if events:
         events["finish_start"].record()
     _check(L.vjp_scan_finish(o, dt, n, _p(as_), _p(ys_bar), _p(ab), _p(ys), _p(ws), nbytes, sh, _p(gathered), s,
@@ -96,7 +116,7 @@ def reduce(op, as_: torch.Tensor, y_bar, *, offset: int, global_n: int, group=No
     _check(L.vjp_reduce_partial(o, dt, n, _p(as_), _p(ws), nbytes, sh, _p(part), s), "vjp_reduce_partial")
     gathered = torch.empty(sh.world * rec, dtype=torch.uint8, device=dev)
     if sh.world > 1:
-        dist.all_gather_into_tensor(gathered, part, group=group)
+        _all_gather_into(gathered, part, group)
     else:
         gathered.copy_(part)
     _check(L.vjp_reduce_finish(o, dt, n, _p(as_), _p(yb), _p(ab), _p(y), _p(arg), _p(ws), nbytes, sh, _p(gathered),
@@ -124,14 +144,14 @@ def reduce_by_index(op, inds: torch.Tensor, as_: torch.Tensor | None, hs_bar: to
                                              _p(bin_aux), s), "vjp_reduce_by_index_partial")
         if sh.world > 1:
             if o == 2:  # MUL
-                dist.all_reduce(bin_val, op=dist.ReduceOp.PRODUCT, group=group)
-                dist.all_reduce(bin_aux, op=dist.ReduceOp.SUM, group=group)
+                _all_reduce(bin_val, dist.ReduceOp.PRODUCT, group)
+                _all_reduce(bin_aux, dist.ReduceOp.SUM, group)
             else:
                 local = bin_val.clone()
-                dist.all_reduce(bin_val, op=dist.ReduceOp.MAX if o == 4 else dist.ReduceOp.MIN, group=group)
+                _all_reduce(bin_val, dist.ReduceOp.MAX if o == 4 else dist.ReduceOp.MIN, group)
                 _check(L.vjp_reduce_by_index_select(o, m, _p(bin_val), _p(local), _p(bin_aux), s),
                        "vjp_reduce_by_index_select")
-                dist.all_reduce(bin_aux, op=dist.ReduceOp.MIN, group=group)
+                _all_reduce(bin_aux, dist.ReduceOp.MIN, group)
     _check(L.vjp_reduce_by_index_finish(o, dt, it, n, m, _p(inds), _p(as_), _p(hs_bar), _p(ab), _p(bin_val),
                                         _p(bin_aux), _p(ws), nbytes, sh, s, ACCUMULATE if accumulate else 0),
            "vjp_reduce_by_index_finish")

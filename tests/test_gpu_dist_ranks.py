@@ -1,0 +1,108 @@
+"""The multi-GPU module (paper_2202_10297_b200.dist) with REAL process groups:
+world_size 2 processes, both on cuda:0 (gpurun exposes one GPU), gloo backend
+for the tiny exchanges (dist routes them through host memory; with NCCL on an
+8-GPU box the same calls use all_gather_into_tensor / all_reduce on device).
+Every rank computes its contiguous shard; rank 0 assembles and checks against
+the oracle on the whole array."""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    try:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+        import oracle
+        import synth
+        from paper_2202_10297_b200 import dist as vdist
+        from _parity import assert_close
+        dev = torch.device("cuda", 0)
+        torch.cuda.set_device(dev)
+        results = {}
+        # scan LINREC / MAT2 / ADD over a global array split in contiguous shards
+        for op, gen, w in (("linrec", synth.linrec_inputs, 2), ("mat2", synth.mat2_inputs, 4),
+                           ("add", None, 1)):
+            N = 300_007
+            off, n = vdist.shard_bounds(N, world, rank)
+            if gen is None:
+                a_l, y_l = None, synth.scan_add_seed(n, offset=off, device=dev)
+            else:
+                a_l, y_l = gen(n, offset=off, device=dev)
+            ab = vdist.scan(op, y_l, a_l, offset=off, global_n=N)
+            parts = [None] * world
+            dist.all_gather_object(parts, ab.cpu().numpy())  # shards differ in size by one element
+            if rank == 0:
+                if gen is None:
+                    a, y = None, synth.scan_add_seed(N)
+                else:
+                    a, y = gen(N)
+                ref = oracle.vjp_scan(op, y.numpy(), None if a is None else a.numpy())
+                assert_close(np.concatenate(parts), ref, np.float64, what=f"2-rank scan {op}")
+        # reduce(min) and reduce(*) with one zero
+        for op in ("min", "mul"):
+            N = 1_000_003
+            off, n = vdist.shard_bounds(N, world, rank)
+            full = synth.min_inputs(N, dtype=torch.float64) if op == "min" else \
+                synth.mul_inputs(N, zeros="one", dtype=torch.float64)
+            ab, y, arg = vdist.reduce(op, full[off:off + n].clone().to(dev), 1.5, offset=off, global_n=N, want_y=True)
+            parts = [None] * world
+            dist.all_gather_object(parts, ab.cpu().numpy())
+            if rank == 0:
+                ref, ry, rarg, _ = oracle.vjp_reduce(op, full.numpy(), 1.5)
+                got = np.concatenate(parts)
+                assert int(arg.item()) == rarg
+                assert_close(got, ref, np.float64, what=f"2-rank reduce {op}")
+        # reduce_by_index (+, *, max)
+        for op, m in (("add", 1000), ("mul", 1000), ("max", 20_000)):
+            N = 500_009
+            off, n = vdist.shard_bounds(N, world, rank)
+            inds, a, hb = synth.rbi_inputs(N, m, op)
+            ab = vdist.reduce_by_index(op, inds[off:off + n].clone().to(dev), a[off:off + n].clone().to(dev),
+                                       hb.to(dev), offset=off, global_n=N)
+            parts = [None] * world
+            dist.all_gather_object(parts, ab.cpu().numpy())
+            if rank == 0:
+                ref = oracle.vjp_reduce_by_index(op, inds.numpy(), a.numpy(), hb.numpy())[0]
+                assert_close(np.concatenate(parts), ref, np.float64, what=f"2-rank rbi {op}")
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception:
+        import traceback
+        q.put((rank, traceback.format_exc()))
+
+
+def test_dist_two_ranks_one_gpu():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    for r in range(world):
+        assert res[r] == "ok", res[r]
