@@ -1,0 +1,32 @@
+"""Small cases of every kernel, run under compute-sanitizer (memcheck / racecheck / synccheck):
+    compute-sanitizer --tool racecheck --error-exitcode 9 python tests/sanitize_cases.py
+"""
+import sys
+sys.path.insert(0, '.')
+import torch, synth, paper_2202_10297_b200 as vjp
+dev = 'cuda'
+for op in ('add', 'mul', 'min', 'max', 'linrec', 'mat2'):
+    for n in (1, 1000, 70_001):
+        w = vjp.WIDTH[vjp.OPS[op]]
+        a = (0.5 + synth.uniform(n * w, 1, device=dev)) if op != 'add' else None
+        yb = synth.uniform(n * w, 2, device=dev)
+        vjp.scan(op, yb, a)
+        if op in ('add', 'mul', 'linrec', 'mat2'):
+            vjp.scan(op, yb, a, lookback=True)
+        if a is not None:
+            vjp.scan(op, yb, a, want_ys=True)
+        vjp.scan(op, yb, a, out=torch.zeros_like(yb), accumulate=True)
+for op in ('add', 'mul', 'min', 'max'):
+    for n in (1, 999, 100_003):
+        a = synth.mul_inputs(n, zeros='one', dtype=torch.float64, device=dev)
+        vjp.reduce(op, a, 1.0, want_y=True)
+        vjp.reduce(op, a, 1.0, out=torch.zeros_like(a), accumulate=True)
+    for n, m in ((5, 3), (10_001, 100), (50_003, 20_000)):
+        inds, a, hb = synth.rbi_inputs(n, m, op, device=dev)
+        vjp.reduce_by_index(op, inds, a, hb, want_hs=True)
+        vjp.reduce_by_index(op, inds, a, hb, out=torch.zeros_like(a), accumulate=True)
+is_, yb = synth.scatter_inputs(10_000, 3000, device=dev)
+vjp.scatter(is_, yb)
+vjp.scatter(is_, yb.clone(), in_place=True)
+torch.cuda.synchronize()
+print('sanitize cases done')
