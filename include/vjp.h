@@ -88,9 +88,13 @@ typedef enum {
 enum {
     VJP_ACCUMULATE = 1u,     /* as_bar += contribution instead of = */
     VJP_CHECK_INDICES = 2u,  /* scatter: detect duplicates / out-of-range (synchronises) */
-    VJP_SCAN_LOOKBACK = 1u << 16 /* tuning/testing: vjp_scan uses the single-sweep decoupled
+    VJP_SCAN_LOOKBACK = 1u << 16, /* tuning/testing: vjp_scan uses the single-sweep decoupled
                                     look-back kernels instead of the chunked reduce-then-scan
                                     kernels (MIN/MAX always use look-back) */
+    VJP_SCAN_SWEEP = 1u << 17     /* tuning/testing (single GPU, ADD/MUL/LINREC/MAT2): one
+                                    persistent kernel that reads as/ys_bar from HBM once and
+                                    re-reads each round from L2 (method bytes); slower than the
+                                    default chunked kernels on B200 */
 };
 
 /* One shard of a multi-GPU call: this process owns global elements

@@ -5,7 +5,10 @@
 #include <mutex>
 #include <type_traits>
 
-#include "scan_chunked.cuh"
+#include <cstdio>
+#include <cstdlib>
+
+#include "scan_sweep.cuh"
 
 namespace vjph {
 
@@ -46,7 +49,7 @@ struct ScanImpl {
         int64_t ntiles;
         size_t counters, flags1, flags2, memset_bytes, p1agg, p1inc, p2agg, p2inc, partial;
         int64_t ntiles_c;
-        size_t tileF, tileP, chunkRec, counter_c, total;
+        size_t tileF, tileP, chunkRec, counter_c, roundRec, arrive, total;
     };
     static Layout layout(int64_t n) {
         Layout L{};
@@ -66,6 +69,9 @@ struct ScanImpl {
         L.tileP = off; off += align256((size_t)L.ntiles_c * W * 8);
         L.chunkRec = off; off += align256((size_t)kMaxChunks * R1MAX * 8);
         L.counter_c = off; off += 256;
+        // sweep: R*G <= ntiles_c/K + G <= ntiles_c + kMaxChunks records; R <= ntiles_c
+        L.roundRec = off; off += align256((size_t)(L.ntiles_c + kMaxChunks) * MD * 8);
+        L.arrive = off; off += align256((size_t)(L.ntiles_c + 1) * 4);
         L.total = off;
         return L;
     }
@@ -273,8 +279,119 @@ struct ScanImpl {
         return !std::is_same<Op, vjpk::OpAdd>::value || c.ys != nullptr;
     }
 
+    // ---------------- single-read L2-round sweep (world == 1) ----------------
+    static constexpr int SW_S_1 = 4;  // TMA stages when a stage is one 16 KB buffer
+    static constexpr int SW_S_2 = 3;  // ... two or three buffers
+
+    static bool use_sweep(const ScanCall &c) {
+        return c.world == 1 && (c.flags & VJP_SCAN_SWEEP) && !(c.flags & VJP_SCAN_LOOKBACK);
+    }
+
+    template <bool FWD, bool ACC, bool YS>
+    static constexpr int sw_stages() { return ((FWD ? 1 : 0) + 1 + (ACC ? 1 : 0)) == 1 ? SW_S_1 : SW_S_2; }
+
+    template <bool FWD, bool ACC, bool YS>
+    static size_t smem_sw() {
+        constexpr int S = sw_stages<FWD, ACC, YS>();
+        constexpr int NBA = (FWD ? 1 : 0) + 1 + (ACC ? 1 : 0);
+        return 1024 + (size_t)S * NBA * NTC * vjpk::kRowBytes + sizeof(vjpk::SweepSmem<Op, S>);
+    }
+
+    // K_F chunking (forward aggregates only) shared by partial and finish
+    static int nchunks_fwd(const Layout &L) {
+        int occ = occupancy(vjpk::scan_reduce<Op, T, NTC, SC, true, false>, smem_r(1));
+        int64_t g = (int64_t)sm_count() * occ;
+        if (g > kMaxChunks) g = kMaxChunks;
+        if (g > L.ntiles_c) g = L.ntiles_c;
+        return (int)(g < 1 ? 1 : g);
+    }
+
+    static vjp_status partial_sw(const ScanCall &c) {
+        if (!need_fwd(c)) return VJP_OK;  // ADD closed form: nothing before the sweep
+        Layout L = layout(c.n);
+        vjpk::ChunkParams p = cparams(c, L, nchunks_fwd(L));
+        CUtensorMap ma, my, mab, mys;
+        if (!maps_c(c, p.full_rows, &ma, &my, &mab, &mys)) return VJP_ECUDA;
+        auto k = vjpk::scan_reduce<Op, T, NTC, SC, true, false>;
+        size_t sm = smem_r(1);
+        set_smem(k, sm);
+        k<<<(unsigned)p.nchunks, NTC, sm, c.stream>>>(ma, my, p);
+        count_launch();
+        return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+    }
+
+    static int env_int(const char *name, int dflt) {
+        const char *v = std::getenv(name);
+        return (v && *v) ? std::atoi(v) : dflt;
+    }
+
+    template <bool FWD, bool ACC, bool YS>
+    static vjp_status launch_sweep(const ScanCall &c, const Layout &L) {
+        constexpr int S = sw_stages<FWD, ACC, YS>();
+        constexpr int NBR = (FWD ? 1 : 0) + 1;
+        constexpr int NTH = NTC + 64;  // four tile warps + producer + carry
+        auto k = vjpk::scan_sweep<Op, T, NTC, S, FWD, ACC, YS, true>;
+        const size_t sm = smem_sw<FWD, ACC, YS>();
+        set_smem(k, sm);
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NTH, sm) != cudaSuccess || occ < 1) occ = 1;
+        vjpk::SweepParams sp{};
+        sp.c = cparams(c, L, 1);
+        int64_t G = (int64_t)sm_count() * occ;
+        if (G > kMaxChunks) G = kMaxChunks;
+        // tiles per CTA per round: about `round_mb` MB of HBM-read input per round
+        const int64_t round_bytes = (int64_t)env_int("VJP_SWEEP_ROUND_MB", 32) << 20;
+        int64_t K = round_bytes / (G * NBR * NTC * vjpk::kRowBytes);
+        K = env_int("VJP_SWEEP_K", (int)K);
+        if (K < 1) K = 1;
+        if (K > vjpk::kSweepKMax) K = vjpk::kSweepKMax;
+        if (G * K > L.ntiles_c) {  // small inputs: fewer, fuller CTAs
+            K = 1;
+            if (G > L.ntiles_c) G = L.ntiles_c;
+        }
+        sp.G = (int32_t)G;
+        sp.K = (int32_t)K;
+        sp.R = (int32_t)((L.ntiles_c + G * K - 1) / (G * K));
+        sp.D = env_int("VJP_SWEEP_D", 1) >= 2 ? 2 : 1;
+        unsigned char *ws = static_cast<unsigned char *>(c.ws);
+        sp.roundRec = reinterpret_cast<double *>(ws + L.roundRec);
+        sp.arrive = reinterpret_cast<uint32_t *>(ws + L.arrive);
+        if (cudaMemsetAsync(sp.arrive, 0, (size_t)sp.R * 4, c.stream) != cudaSuccess) return VJP_ECUDA;
+        CUtensorMap ma, my, mab, mys, mab32, mys32;
+        if (!maps_c(c, sp.c.full_rows, &ma, &my, &mab, &mys)) return VJP_ECUDA;
+        const bool f64 = sizeof(T) == 8;
+        if (!make_row_tmap(&mab32, c.as_bar, sp.c.full_rows, f64, 32)) return VJP_ECUDA;
+        if (!make_row_tmap(&mys32, c.ys, c.ys ? sp.c.full_rows : 0, f64, 32)) return VJP_ECUDA;
+        if (env_int("VJP_SWEEP_DEBUG", 0))
+            fprintf(stderr, "vjp sweep: occ=%d G=%d K=%d R=%d D=%d smem=%zu ntiles=%lld\n", occ, sp.G, sp.K, sp.R, sp.D, sm,
+                    (long long)L.ntiles_c);
+        void *args[] = {&ma, &my, &mab, &mab32, &mys32, &sp};
+        cudaError_t e = cudaLaunchCooperativeKernel((const void *)k, dim3((unsigned)G), dim3(NTH), args, sm, c.stream);
+        count_launch();
+        return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+    }
+
+    static vjp_status finish_sw(const ScanCall &c) {
+        Layout L = layout(c.n);
+        const bool fwd = need_fwd(c);
+        const bool acc = (c.flags & VJP_ACCUMULATE) != 0;
+        const bool ys = c.ys != nullptr;
+        if (fwd) {
+            vjpk::ChunkParams p = cparams(c, L, nchunks_fwd(L));
+            vjpk::scan_tile_prefix<Op, NTC><<<(unsigned)p.nchunks, NTC, 0, c.stream>>>(p);
+            count_launch();
+            if (cudaGetLastError() != cudaSuccess) return VJP_ECUDA;
+        }
+        if constexpr (std::is_same<Op, vjpk::OpAdd>::value) {
+            if (!ys) return acc ? launch_sweep<false, true, false>(c, L) : launch_sweep<false, false, false>(c, L);
+        }
+        if (acc) return ys ? launch_sweep<true, true, true>(c, L) : launch_sweep<true, true, false>(c, L);
+        return ys ? launch_sweep<true, false, true>(c, L) : launch_sweep<true, false, false>(c, L);
+    }
+
     static vjp_status partial(const ScanCall &c) {
         if constexpr (!Op::kRevNeedsRs) {
+            if (use_sweep(c)) return partial_sw(c);
             if (use_chunked(c)) return partial_c(c);
         }
         Layout L = layout(c.n);
@@ -296,6 +413,7 @@ struct ScanImpl {
 
     static vjp_status finish(const ScanCall &c) {
         if constexpr (!Op::kRevNeedsRs) {
+            if (use_sweep(c)) return finish_sw(c);
             if (use_chunked(c)) return finish_c(c);
         }
         Layout L = layout(c.n);

@@ -46,10 +46,10 @@ def make(op, n, dt, device="cpu"):
     raise ValueError(op)
 
 
-def run_both(op, n, dt, lookback=False):
+def run_both(op, n, dt, lookback=False, sweep=False):
     a, yb = make(op, n, dt)
     ref = oracle.vjp_scan(op, yb.numpy(), None if a is None else a.numpy())
-    got = vjp.scan(op, yb.to(DEV), None if a is None else a.to(DEV), lookback=lookback)
+    got = vjp.scan(op, yb.to(DEV), None if a is None else a.to(DEV), lookback=lookback, sweep=sweep)
     torch.cuda.synchronize()
     return got.cpu().numpy(), ref
 
@@ -72,12 +72,46 @@ def test_scan_parity_lookback_path(op):
 
 
 @pytest.mark.parametrize("dt", [np.float64, np.float32], ids=["f64", "f32"])
+@pytest.mark.parametrize("op", ["add", "mul", "linrec", "mat2"])
+def test_scan_parity_sweep_path(op, dt):
+    """the one-read L2-round sweep (VJP_SCAN_SWEEP): rounds of G*K tiles,
+    producer / carry warps, per-warp TMA stores; sizes from one partial tile to
+    many rounds (1 tile per CTA per round at these sizes)."""
+    for n in (1, 33, 1023, 4097, 100_003, 1_000_001, 3_000_017):
+        got, ref = run_both(op, n, dt, sweep=True)
+        assert_close(got, ref, dt, what=f"sweep {op} n={n}")
+
+
+@pytest.mark.parametrize("op", ["add", "linrec"])
+def test_scan_sweep_accumulate_ys_and_rounds(op, monkeypatch):
+    """sweep with ACCUMULATE and with ys, and with several tiles per CTA per
+    round and a 2-round look-ahead (VJP_SWEEP_K / VJP_SWEEP_D)."""
+    n = 2_000_003
+    a, yb = make(op, n, np.float64)
+    if a is None:
+        a = synth.uniform(n, 11, dtype=torch.float64)
+    base = synth.uniform(n * WIDTH[op], 12, dtype=torch.float64)
+    ref_acc = oracle.vjp_scan(op, yb.numpy(), a.numpy(), out=base.numpy().copy(), accumulate=True)
+    ref, ref_ys = oracle.vjp_scan(op, yb.numpy(), a.numpy(), want_ys=True)
+    for k, d in (("", ""), ("3", "1"), ("8", "2")):
+        monkeypatch.setenv("VJP_SWEEP_K", k)
+        monkeypatch.setenv("VJP_SWEEP_D", d)
+        out = base.to(DEV)
+        vjp.scan(op, yb.to(DEV), a.to(DEV), out=out, accumulate=True, sweep=True)
+        assert_close(out.cpu().numpy(), ref_acc, np.float64, what=f"sweep acc {op} K={k} D={d}")
+        got, ys = vjp.scan(op, yb.to(DEV), a.to(DEV), want_ys=True, sweep=True)
+        assert_close(got.cpu().numpy(), ref, np.float64, what=f"sweep {op} K={k} D={d}")
+        if op == "add":
+            assert_close(ys.cpu().numpy(), ref_ys, np.float64, what=f"sweep ys {op}")
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32], ids=["f64", "f32"])
 def test_scan_add_integer_seeds_bit_exact(dt):
     """integer seeds in [-8, 8]: every summation order is exact."""
     for n in (10_000, 1 << 20, (1 << 20) + 3, 5_000_011):
         yb = synth.scan_add_seed(n, kind="int", dtype=TD[dt])
         ref = oracle.vjp_scan("add", yb.numpy(), None)
-        for kw in ({}, {"lookback": True}):
+        for kw in ({}, {"lookback": True}, {"sweep": True}):
             got = vjp.scan("add", yb.to(DEV), **kw).cpu().numpy()
             assert np.array_equal(got, ref), kw
 
@@ -161,6 +195,9 @@ def test_scan_add_2pow30_sampled():
     got = vjp.scan("add", yb)
     exact = torch.flip(torch.cumsum(torch.flip(yb.to(torch.int64), [0]), 0), [0])
     assert torch.equal(got.to(torch.int64), exact)
+    got_sw = vjp.scan("add", yb, sweep=True)  # many rounds of the L2-round sweep
+    assert torch.equal(got_sw.to(torch.int64), exact)
+    del got_sw
     # sampled comparison against the oracle on a slice near the end (independent of the prefix)
     tail = yb[-100_000:].cpu().numpy()
     ref_tail = oracle.vjp_scan("add", tail, None)
