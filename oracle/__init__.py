@@ -52,6 +52,7 @@ def lib():
         L.oracle_vjp_reduce.argtypes = [ci, ci, i64, vp, vp, vp, vp, vp, vp, u32]
         L.oracle_vjp_reduce_by_index.argtypes = [ci, ci, ci, i64, i64, vp, vp, vp, vp, vp, vp, vp, u32]
         L.oracle_vjp_scatter.argtypes = [ci, ci, i64, i64, i64, vp, vp, vp, vp, u32]
+        L.oracle_kmeans.argtypes = [ci, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp]
         for f in (L.oracle_vjp_scan, L.oracle_vjp_reduce, L.oracle_vjp_reduce_by_index,
                   L.oracle_vjp_scatter):
             f.restype = ci
@@ -164,3 +165,31 @@ def vjp_scatter(is_: np.ndarray, ys_bar: np.ndarray, *, width: int = 1, vs_out=N
     if rc not in (0, EDUPINDEX):
         raise RuntimeError(f"oracle_vjp_scatter rc={rc}")
     return xs_bar, vs_bar, rc
+
+
+def kmeans(points: np.ndarray, centers: np.ndarray, cost_bar: float = 1.0):
+    """k-means cost f(C) = sum_p min_j ||p - c_j||^2 and its derivatives by the
+    literal per-point loop (oracle.c; reading R15).
+    points [n x d], centers [k x d] (same dtype).  Returns a dict with
+    cost, cbar [k x d] (vjp with cost_bar), hdiag [k x d] (jvp of the vjp in the
+    all-ones direction = Hessian diagonal), assign int32 [n], counts int64 [k]."""
+    points = np.ascontiguousarray(points)
+    centers = np.ascontiguousarray(centers)
+    if points.ndim != 2 or centers.ndim != 2 or points.shape[1] != centers.shape[1]:
+        raise ValueError("points [n x d] and centers [k x d]")
+    if points.dtype != centers.dtype:
+        raise ValueError("points and centers must share a dtype")
+    n, d = points.shape
+    k = centers.shape[0]
+    dt = _dt(centers)
+    yb = np.array([cost_bar], dtype=centers.dtype)
+    cbar = np.zeros((k, d), dtype=centers.dtype)
+    hdiag = np.zeros((k, d), dtype=centers.dtype)
+    assign = np.zeros(n, dtype=np.int32)
+    counts = np.zeros(k, dtype=np.int64)
+    cost = np.zeros(1, dtype=centers.dtype)
+    rc = lib().oracle_kmeans(dt, n, k, d, _p(points) if n else None, _p(centers), _p(yb), _p(cbar),
+                             _p(hdiag), _p(assign), _p(counts), _p(cost))
+    if rc != 0:
+        raise RuntimeError(f"oracle_kmeans rc={rc}")
+    return {"cost": float(cost[0]), "cbar": cbar, "hdiag": hdiag, "assign": assign, "counts": counts}

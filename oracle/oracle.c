@@ -31,6 +31,12 @@
  *                   products forward and backward).
  *   scatter         P:1274-1275: vs_bar += gather is ys_bar;
  *                   xs_bar = scatter ys_bar is (replicate m 0).
+ *   kmeans          SURVEY 8f row f3 / P:1663-1720: f(C) = sum_p min_j ||p - c_j||^2
+ *                   (reading R15: squared distance), its vjp (reduce(+) adjoint,
+ *                   the min-reduce sparse adjoint with the FIRST index, the map's
+ *                   vjp 2(c - p) accumulated per center) and the jvp of that vjp
+ *                   in the all-ones direction (the Hessian diagonal),
+ *                   all by the literal per-point loop.
  *
  * Readings of the paper where it is silent or garbled:
  *   R1 MAT2 scan order R_i = R_{i-1} . A_i (P:1137 semantics of scan).
@@ -432,4 +438,67 @@ int oracle_vjp_scatter(int dtype, int itype, int64_t n, int64_t m, int64_t width
     }
     free(seen);
     return dup ? O_EDUPINDEX : O_OK;
+}
+
+/*
+ * k-means cost and its derivatives.
+ *
+ *   f(C) = sum_p min_j dist(p, j),  dist(p, j) = sum_t (p_t - c_jt)^2
+ *
+ * (P:1687 writes ||p - c||; reading R15 takes the SQUARED distance, the only
+ * reading with the diagonal Hessian the paper relies on.)
+ * Forward, literally: for every point the distance to every center, then the
+ * min-reduce with the FIRST index among equal minima (strict '<' in a
+ * left-to-right loop), then the +-reduce over points.
+ * Return sweep with cost_bar = ybar, Eq. 3 applied statement by statement:
+ *   y_p bar = ybar (reduce(+));
+ *   dist(p, j) bar = y_p bar if j == a(p), else 0 (reduce(min));
+ *   c_jt bar += dist(p, j) bar * 2 (c_jt - p_t)  (the map's vjp; accumulated
+ *   over p in index order).
+ * jvp of that vjp in the direction cdot = 1 (all ones; ybar, P fixed): the
+ * tangent of c_jt bar is sum_p dist(p, j) bar * 2 * cdot_jt = 2 ybar cnt_j,
+ * which is the Hessian diagonal since the Hessian is diagonal.
+ * Outputs (nullable except Cbar): Cbar, H [k x d]; assign int32 [n];
+ * counts int64 [k]; cost [1].  Arrays are row-major [rows x d].
+ */
+int oracle_kmeans(int dtype, int64_t n, int64_t k, int64_t d, const void *P, const void *C,
+                  const void *cost_bar, void *Cbar, void *H, int32_t *assign, int64_t *counts,
+                  void *cost) {
+    if ((dtype != O_F32 && dtype != O_F64) || n < 0 || k < 1 || d < 1) return O_EINVAL;
+    if ((n > 0 && !P) || !C || !cost_bar || !Cbar) return O_EINVAL;
+    const LD ybar = ld_get(dtype, cost_bar, 0);
+    LD *g = (LD *)calloc((size_t)(k * d), sizeof(LD));
+    int64_t *cnt = (int64_t *)calloc((size_t)k, sizeof(int64_t));
+    if (!g || !cnt) { free(g); free(cnt); return O_EINVAL; }
+    LD total = 0.0L;
+    for (int64_t p = 0; p < n; ++p) {
+        /* forward: distances and the first-index argmin */
+        int64_t a = -1;
+        LD best = 0.0L;
+        for (int64_t j = 0; j < k; ++j) {
+            LD dist = 0.0L;
+            for (int64_t t = 0; t < d; ++t) {
+                LD diff = ld_get(dtype, P, p * d + t) - ld_get(dtype, C, j * d + t);
+                dist += diff * diff;
+            }
+            if (a < 0 || dist < best) { best = dist; a = j; }
+        }
+        total += best;
+        if (assign) assign[p] = (int32_t)a;
+        cnt[a] += 1;
+        /* return sweep of this point: only the argmin center receives an adjoint */
+        for (int64_t t = 0; t < d; ++t)
+            g[a * d + t] += ybar * 2.0L * (ld_get(dtype, C, a * d + t) - ld_get(dtype, P, p * d + t));
+    }
+    for (int64_t j = 0; j < k; ++j) {
+        for (int64_t t = 0; t < d; ++t) {
+            ld_put(dtype, Cbar, j * d + t, g[j * d + t], 0);
+            if (H) ld_put(dtype, H, j * d + t, 2.0L * ybar * (LD)cnt[j], 0);
+        }
+        if (counts) counts[j] = cnt[j];
+    }
+    if (cost) ld_put(dtype, cost, 0, total, 0);
+    free(g);
+    free(cnt);
+    return O_OK;
 }

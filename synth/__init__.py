@@ -182,3 +182,30 @@ def scatter_inputs(n, m, *, dtype=torch.float64, itype=torch.int64, device="cpu"
         is_[:oob] = n + torch.arange(oob, device=device) * 7 + 1
     ybar = uniform(n, 500, lo=-1.0, hi=1.0, dtype=dtype, device=device)
     return is_.to(itype), ybar
+
+
+def _normal40(n, stream0, *, offset=0, device="cpu"):
+    """N(0,1)-shaped noise without transcendental functions (Irwin-Hall): the
+    sum of 12 U[0,1) with 40 random bits each, minus 6.  Every term is a
+    multiple of 2^-40 below 1, so the sum is exact in f64 and CPU/CUDA agree
+    bit for bit."""
+    acc = torch.zeros(n, dtype=torch.float64, device=device)
+    for t in range(12):
+        acc += _srl(bits(n, stream0 + t, offset=offset, device=device), 24).to(torch.float64) * (2.0 ** -40)
+    return acc - 6.0
+
+
+def kmeans_inputs(n, k, d, *, dtype=torch.float64, offset=0, device="cpu", k_true=None):
+    """config 5 (composite k-means gradient): points from a mixture of k_true
+    (default k) Gaussian clusters: true centres U(-10, 10)^d, cluster ids i.i.d.
+    uniform, unit noise (Irwin-Hall); the current centers C = true centres +
+    0.1 * noise.  Row-major [n x d] points, [k x d] centers.  `offset` shifts
+    the point index (shards of a multi-GPU run are slices of the 1-GPU arrays)."""
+    kt = k if k_true is None else k_true
+    centres = uniform(kt * d, 600, lo=-10.0, hi=10.0, device=device).reshape(kt, d)
+    ids = integers(n, 601, 0, kt - 1, offset=offset, device=device)
+    noise = _normal40(n * d, 610, offset=offset * d, device=device).reshape(n, d)
+    points = centres[ids] + noise
+    cnoise = _normal40(k * d, 630, device=device).reshape(k, d)
+    centers = centres[torch.arange(k, device=device) % kt] + 0.1 * cnoise
+    return points.to(dtype).contiguous(), centers.to(dtype).contiguous()
