@@ -291,6 +291,36 @@ vjp_status vjp_scatter(vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, i
                        const void *is, const void *ys_bar, void *xs_bar, void *vs_bar, void *ws,
                        size_t ws_bytes, vjp_stream_t stream, unsigned flags);
 
+/* ======================================================================
+ * vjp_kmeans — composite k-means cost gradient (BASELINE
+ * config 5)
+ *
+ * f(C) = sum_p min_j ||p - c_j||^2 (reading R15: squared distance; ties go
+ * to the FIRST center).  One call runs the forward (distances,
+ * argmin, cost) and the return sweep with cost_bar = ybar:
+ *   centers_bar[j] = 2 ybar sum_{p: a(p) = j} (c_j - p)
+ * — the sum's adjoint, the min's sparse adjoint (only the
+ * argmin's distance receives ybar) and the distance map's vjp,
+ * accumulated per center as a width-d reduce_by_index(+) into k bins
+ * (done as a stable counting sort + in-order segmented sum, so
+ * the result is deterministic) — and the jvp of that vjp in the all-ones
+ * direction, the Hessian diagonal hess_diag[j][t] = 2 ybar cnt_j.
+ *   points  [n x d] row-major, centers [k x d]; f32 or f64 (arithmetic f64).
+ *   cost_bar DEVICE [1].  centers_bar [k x d] output.
+ *   hess_diag, assign (int32 [n]), counts (int64 [k]), cost ([1]): nullable
+ *   DEVICE outputs.  VJP_ACCUMULATE adds into centers_bar, hess_diag, counts
+ *   and cost (per-shard partials of a multi-GPU run are sums over points).
+ * Limits: n < 2^31, 1 <= k <= 12288 (VJP_EUNSUPPORTED beyond), d >= 1.
+ * Errors: VJP_EINVAL, VJP_EALIGN (element misalignment), VJP_EWORKSPACE,
+ * VJP_ECUDA.  The workspace holds per-center/per-block tables and two int32
+ * arrays of n (point order, assignment when `assign` is NULL).
+ * ==================================================================== */
+size_t vjp_kmeans_workspace_bytes(vjp_dtype dtype, int64_t n, int64_t k, int64_t d);
+vjp_status vjp_kmeans(vjp_dtype dtype, int64_t n, int64_t k, int64_t d, const void *points,
+                      const void *centers, const void *cost_bar, void *centers_bar, void *hess_diag,
+                      int32_t *assign, int64_t *counts, void *cost, void *ws, size_t ws_bytes,
+                      vjp_stream_t stream, unsigned flags);
+
 #ifdef __cplusplus
 }
 #endif

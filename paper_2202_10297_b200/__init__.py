@@ -78,6 +78,8 @@ def lib():
             "vjp_reduce_by_index_finish": ([ci, ci, ci, i64, i64, vp, vp, vp, vp, vp, vp, vp, sz, sp, vp, u32], ci),
             "vjp_scatter_workspace_bytes": ([ci, i64, i64], sz),
             "vjp_scatter": ([ci, ci, i64, i64, i64, vp, vp, vp, vp, vp, sz, vp, u32], ci),
+            "vjp_kmeans_workspace_bytes": ([ci, i64, i64, i64], sz),
+            "vjp_kmeans": ([ci, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, u32], ci),
         }
         for name, (args, res) in sig.items():
             if not hasattr(L, name):
@@ -306,3 +308,50 @@ def scatter(is_: torch.Tensor, ys_bar: torch.Tensor, *, width: int = 1, in_place
     _check(L.vjp_scatter(_dt(yb), _it(ix), n, m, width, _p(ix), _p(yb), _p(xb), _p(vb), _p(ws),
                          0 if ws is None else ws.numel(), _stream(dev), flags), "vjp_scatter")
     return _host_out(xb, host), _host_out(vb, host)
+
+
+def kmeans(points: torch.Tensor, centers: torch.Tensor, cost_bar=1.0, *, hess: bool = True,
+           accumulate: bool = False, out: dict | None = None):
+    """Composite k-means gradient (SURVEY 8f row f3, BASELINE config 5;
+    P:1663-1720): for f(C) = sum_p min_j ||p - c_j||^2, returns a dict with
+    ``cbar`` (vjp of f at C with cost_bar), ``hdiag`` (jvp of that vjp in the
+    all-ones direction = the Hessian diagonal 2 cost_bar cnt_j; if hess),
+    ``assign`` (int32 first-index argmin per point), ``counts`` (int64 [k]) and
+    ``cost`` (0-d tensor).  points [n x d], centers [k x d], f32 or f64 (the
+    arithmetic is f64).  ``out`` may hold preallocated device tensors under the
+    same keys (accumulate adds into cbar / hdiag / counts / cost)."""
+    dev = _dev_of(points, centers)
+    P = _to(points, dev)
+    C = _to(centers, dev)
+    if P.dim() != 2 or C.dim() != 2 or P.shape[1] != C.shape[1] or P.dtype != C.dtype:
+        raise ValueError("kmeans: points [n x d] and centers [k x d] of one dtype")
+    n, d = P.shape
+    k = C.shape[0]
+    if not torch.is_tensor(cost_bar):
+        cost_bar = torch.tensor([float(cost_bar)], dtype=C.dtype)
+    yb = _to(cost_bar.reshape(1).to(C.dtype), dev)
+    o = dict(out or {})
+    cbar = o.get("cbar")
+    if cbar is None:
+        cbar = torch.empty_like(C) if not accumulate else torch.zeros_like(C)
+    hd = o.get("hdiag")
+    if hess and hd is None:
+        hd = torch.empty_like(C) if not accumulate else torch.zeros_like(C)
+    asg = o.get("assign")
+    if asg is None or asg.numel() != n:
+        asg = torch.empty(n, dtype=torch.int32, device=dev)
+    for key, t, numel in (("cbar", cbar, k * d), ("hdiag", hd, k * d), ("counts", o.get("counts"), k)):
+        if t is not None and t.numel() != numel:
+            raise ValueError(f"kmeans: out[{key!r}] has {t.numel()} elements, expected {numel}")
+    cnt = o.get("counts")
+    if cnt is None:
+        cnt = torch.zeros(k, dtype=torch.int64, device=dev)
+    cost = o.get("cost")
+    if cost is None:
+        cost = torch.zeros((), dtype=C.dtype, device=dev)
+    L = lib()
+    ws = workspace(L.vjp_kmeans_workspace_bytes(_dt(C), n, k, d), dev)
+    _check(L.vjp_kmeans(_dt(C), n, k, d, _p(P), _p(C), _p(yb), _p(cbar), _p(hd), _p(asg), _p(cnt), _p(cost),
+                        _p(ws), 0 if ws is None else ws.numel(), _stream(dev), ACCUMULATE if accumulate else 0),
+           "vjp_kmeans")
+    return {"cbar": cbar, "hdiag": hd, "assign": asg, "counts": cnt, "cost": cost}

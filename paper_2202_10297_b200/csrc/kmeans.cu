@@ -1,0 +1,510 @@
+// kmeans.cu — composite k-means cost gradient (BASELINE
+// config 5) for sm_100a.
+//
+//   f(C) = sum_p min_j ||p - c_j||^2        (reading R15: squared distance)
+//
+// Forward (compute bound, FP64 FMA):
+//   km_cnorm   ||c_j||^2
+//   km_assign  register-tiled distance expansion ||c_j||^2 - 2 p.c_j per point
+//              and center (128 points x 64 centers per CTA, 8 x 8 per thread,
+//              smem tiles of 32 dimensions), the FIRST-index argmin per point
+//               and the per-point minimum distance (cost).
+// Return sweep with cost_bar = ybar (vjp; P:1034-1038 for the sum over points,
+// P:1071-1087 for the min's sparse adjoint — only dist(p, a(p)) gets ybar —
+// and the map's vjp 2 (c_a - p)), its accumulation per center being a
+// reduce_by_index(+) of width d into k bins: realised as a
+// STABLE counting sort of the points by center followed by an in-order
+// segmented sum, so the result is deterministic (no floating-point atomics):
+//   km_hist      per block of 4096 points, per-center counts (smem 32-bit atomics)
+//   km_colscan   per center, exclusive scan over the blocks (column of the table)
+//   km_startscan exclusive scan of the per-center totals -> segment starts
+//   km_order     stable ranks (warp match_any per 32 points, in index order)
+//                -> order[] = point indices grouped by center, increasing
+//   km_segsum    one warp per center: C_bar_j = 2 ybar sum_{p in j} (c_j - p)
+//                in index order (rows gathered 16 at a time, coalesced per row);
+//                Hessian diagonal (jvp of the vjp, all-ones direction,
+//                P:1696-1700) H_j = 2 ybar cnt_j.
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace vjpk {
+
+constexpr int KM_BP = 128;   // points per assign CTA
+constexpr int KM_BC = 64;    // centers per tile
+constexpr int KM_KD = 32;    // dimensions per smem stage
+constexpr int KM_NT = 128;   // assign threads (16 x 8 grid of 8 x 8 tiles)
+constexpr int KM_BH = 4096;  // points per histogram block
+constexpr int KM_SEGB = 16;  // rows gathered per batch in km_segsum
+
+// position of point pp (0..127) / center cc (0..63) in the swizzled smem rows:
+// thread tp owns points tp*8 .. tp*8+7 and reads them as 4 x 16 B at
+// q*32 + tp*2 (conflict free); thread tc owns centers tc*8 .. tc*8+7 at q*16 + tc*2
+__device__ __forceinline__ int km_ppos(int pp) { return ((pp & 7) >> 1) * 32 + (pp >> 3) * 2 + (pp & 1); }
+__device__ __forceinline__ int km_cpos(int cc) { return ((cc & 7) >> 1) * 16 + (cc >> 3) * 2 + (cc & 1); }
+
+template <class T>
+__global__ void km_cnorm(const T *__restrict__ C, int64_t k, int64_t d, double *__restrict__ cn) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= k) return;
+    double s = 0.0;
+    for (int64_t t = 0; t < d; ++t) {
+        const double v = (double)C[j * d + t];
+        s = fma(v, v, s);
+    }
+    cn[j] = s;
+}
+
+// one element of a stage: f64 by an 8-byte cp.async (zero-filled when out of
+// range), f32 through a register (converted to f64)
+__device__ __forceinline__ void km_stage(double *dst, const double *src, bool ok) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(ok ? src : nullptr), "r"(ok ? 8 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void km_stage(double *dst, const float *src, bool ok) { *dst = ok ? (double)*src : 0.0; }
+__device__ __forceinline__ void km_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void km_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Dynamic shared memory: Ps [DP][128] point tile (dim-major, swizzled), resident
+// for the whole CTA when d <= 64 (DP = d rounded up to 32), else one 32-dim
+// chunk re-staged per stage; Cs [2][32][64] double-buffered center chunks.
+// Stage s = (center tile s / nd, dim chunk s % nd), prefetched one ahead.
+template <class T, bool RES>
+__global__ void __launch_bounds__(KM_NT, 2) km_assign(const T *__restrict__ P, const T *__restrict__ C,
+                                                      const double *__restrict__ cn, int64_t n, int64_t k,
+                                                      int64_t d, int32_t *__restrict__ assign,
+                                                      double *__restrict__ cost_part) {
+    extern __shared__ __align__(16) double km_smem[];
+    const int nd = (int)((d + KM_KD - 1) / KM_KD);
+    const int DP = RES ? nd * KM_KD : 2 * KM_KD;        // rows of Ps
+    double *Ps = km_smem;                                // [DP][KM_BP]
+    double *Cs = km_smem + (size_t)DP * KM_BP;           // [2][KM_KD][KM_BC]
+    const int t = threadIdx.x, tp = t & 15, tc = t >> 4;
+    const int64_t p0 = (int64_t)blockIdx.x * KM_BP;
+    const int nct = (int)((k + KM_BC - 1) / KM_BC), nst = nct * nd;
+
+    auto stage = [&](int st) {
+        const int ct = st / nd, dc = st % nd, buf = st & 1;
+        const int64_t c0 = (int64_t)ct * KM_BC, d0 = (int64_t)dc * KM_KD;
+        double *cs = Cs + (size_t)buf * KM_KD * KM_BC;
+#pragma unroll 4
+        for (int idx = t; idx < KM_BC * KM_KD; idx += KM_NT) {
+            const int cc = idx / KM_KD, kk = idx % KM_KD;
+            const int64_t gc = c0 + cc, gd = d0 + kk;
+            const bool ok = gc < k && gd < d;
+            km_stage(cs + kk * KM_BC + km_cpos(cc), C + (ok ? gc * d + gd : 0), ok);
+        }
+        if (!RES) {
+            double *ps = Ps + (size_t)buf * KM_KD * KM_BP;
+#pragma unroll 4
+            for (int idx = t; idx < KM_BP * KM_KD; idx += KM_NT) {
+                const int pp = idx / KM_KD, kk = idx % KM_KD;
+                const int64_t gp = p0 + pp, gd = d0 + kk;
+                const bool ok = gp < n && gd < d;
+                km_stage(ps + kk * KM_BP + km_ppos(pp), P + (ok ? gp * d + gd : 0), ok);
+            }
+        }
+        km_commit();
+    };
+
+    if (RES) {  // the whole point tile, once
+#pragma unroll 4
+        for (int idx = t; idx < KM_BP * DP; idx += KM_NT) {
+            const int pp = idx / DP, kk = idx % DP;
+            const int64_t gp = p0 + pp;
+            const bool ok = gp < n && kk < d;
+            km_stage(Ps + kk * KM_BP + km_ppos(pp), P + (ok ? gp * d + kk : 0), ok);
+        }
+    }
+    stage(0);  // (commits the resident tile with it)
+
+    double bv[8];
+    int32_t bj[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        bv[i] = INFINITY;
+        bj[i] = 0x7fffffff;
+    }
+    double pnorm = 0.0;  // ||p_{p0+t}||^2, accumulated during center tile 0
+    double acc[8][8];
+    for (int st = 0; st < nst; ++st) {
+        const int ct = st / nd, dc = st % nd;
+        if (dc == 0) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+        }
+        if (st + 1 < nst) {
+            __syncthreads();  // buffer (st+1)&1 was consumed at stage st-1
+            stage(st + 1);
+            km_wait<1>();
+        } else {
+            km_wait<0>();
+        }
+        __syncthreads();
+        const double *ps = RES ? Ps + (size_t)dc * KM_KD * KM_BP : Ps + (size_t)(st & 1) * KM_KD * KM_BP;
+        const double *cs = Cs + (size_t)(st & 1) * KM_KD * KM_BC;
+        if (ct == 0) {
+#pragma unroll 8
+            for (int kk = 0; kk < KM_KD; ++kk) {
+                const double v = ps[kk * KM_BP + km_ppos(t)];
+                pnorm = fma(v, v, pnorm);
+            }
+        }
+#pragma unroll 2
+        for (int kk = 0; kk < KM_KD; ++kk) {
+            double a[8], b[8];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const double2 va = *reinterpret_cast<const double2 *>(ps + kk * KM_BP + q * 32 + tp * 2);
+                const double2 vb = *reinterpret_cast<const double2 *>(cs + kk * KM_BC + q * 16 + tc * 2);
+                a[2 * q] = va.x;
+                a[2 * q + 1] = va.y;
+                b[2 * q] = vb.x;
+                b[2 * q + 1] = vb.y;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        }
+        if (dc == nd - 1) {
+            // candidates: ||c_j||^2 - 2 p.c_j (||p||^2 is common to a point's candidates)
+            const int64_t c0 = (int64_t)ct * KM_BC;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int64_t gc = c0 + tc * 8 + j;
+                if (gc < k) {
+                    const double cnj = cn[gc];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const double v = fma(-2.0, acc[i][j], cnj);
+                        if (v < bv[i] || (v == bv[i] && (int32_t)gc < bj[i])) {
+                            bv[i] = v;
+                            bj[i] = (int32_t)gc;
+                        }
+                    }
+                }
+            }
+        }
+    }
+    // combine the 8 center columns of each point (first index on ties);
+    // the epilogue scratch reuses the center buffers
+    __syncthreads();
+    double *rv = Cs;                                        // [8][128]
+    int32_t *rj = reinterpret_cast<int32_t *>(Cs + 8 * KM_BP);  // [8][128]
+    double *pn = Cs + 12 * KM_BP;                           // [128]
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        rv[tc * KM_BP + tp * 8 + i] = bv[i];
+        rj[tc * KM_BP + tp * 8 + i] = bj[i];
+    }
+    pn[t] = pnorm;
+    __syncthreads();
+    double md = 0.0;
+    {
+        const int pp = t;  // one point per thread
+        double v = rv[pp];
+        int32_t j = rj[pp];
+#pragma unroll
+        for (int c = 1; c < 8; ++c) {
+            const double w = rv[c * KM_BP + pp];
+            const int32_t jw = rj[c * KM_BP + pp];
+            if (w < v || (w == v && jw < j)) {
+                v = w;
+                j = jw;
+            }
+        }
+        const int64_t gp = p0 + pp;
+        if (gp < n) {
+            assign[gp] = j;
+            md = fmax(pn[pp] + v, 0.0);
+        }
+    }
+    // per-CTA cost partial, fixed order (deterministic)
+    for (int o = 16; o > 0; o >>= 1) md += __shfl_down_sync(0xffffffffu, md, o);
+    __syncthreads();
+    if ((t & 31) == 0) rv[t >> 5] = md;
+    __syncthreads();
+    if (t == 0) cost_part[blockIdx.x] = ((rv[0] + rv[1]) + rv[2]) + rv[3];
+}
+
+__global__ void km_hist(const int32_t *__restrict__ assign, int64_t n, int64_t k, int32_t *__restrict__ hist) {
+    extern __shared__ int32_t h[];
+    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) h[j] = 0;
+    __syncthreads();
+    const int64_t b0 = (int64_t)blockIdx.x * KM_BH;
+    for (int64_t i = b0 + threadIdx.x; i < b0 + KM_BH && i < n; i += blockDim.x) atomicAdd(h + assign[i], 1);
+    __syncthreads();
+    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) hist[(int64_t)blockIdx.x * k + j] = h[j];
+}
+
+// per center (column): exclusive scan over the blocks in place, column total
+__global__ void km_colscan(int32_t *__restrict__ hist, int64_t nb, int64_t k, int32_t *__restrict__ colsum) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= k) return;
+    int32_t s = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        const int32_t v = hist[b * k + j];
+        hist[b * k + j] = s;
+        s += v;
+    }
+    colsum[j] = s;
+}
+
+// exclusive scan of the column totals (one CTA of 1024 threads): start[j], start[k] = n
+__global__ void __launch_bounds__(1024) km_startscan(const int32_t *__restrict__ colsum, int64_t k,
+                                                     int32_t *__restrict__ start, int64_t *__restrict__ counts,
+                                                     int acc_counts) {
+    __shared__ int32_t wsum[32];
+    __shared__ int32_t carry;
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    if (t == 0) carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < k; base += 1024) {
+        const int64_t j = base + t;
+        const int32_t v = j < k ? colsum[j] : 0;
+        int32_t x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            int32_t s = wsum[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t y = __shfl_up_sync(0xffffffffu, s, o);
+                if (lane >= o) s += y;
+            }
+            wsum[lane] = s;  // inclusive over warps
+        }
+        __syncthreads();
+        const int32_t excl = carry + (w ? wsum[w - 1] : 0) + x - v;
+        if (j < k) {
+            start[j] = excl;
+            if (counts) counts[j] = (acc_counts ? counts[j] : 0) + v;
+        }
+        __syncthreads();
+        if (t == 1023) carry = excl + v;
+        __syncthreads();
+    }
+    if (t == 0) start[k] = carry;
+}
+
+// stable counting-sort scatter: one warp per block of KM_BH points, in index order
+__global__ void km_order(const int32_t *__restrict__ assign, int64_t n, int64_t k, const int32_t *__restrict__ hist,
+                         const int32_t *__restrict__ start, int32_t *__restrict__ order, int64_t nb) {
+    extern __shared__ int32_t cnt[];  // [warps][k]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int64_t b = (int64_t)blockIdx.x * nw + w;
+    int32_t *c = cnt + (int64_t)w * k;
+    for (int64_t j = lane; j < k; j += 32) c[j] = 0;
+    __syncwarp();
+    if (b >= nb) return;
+    const int64_t b0 = b * KM_BH;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int64_t i0 = b0; i0 < b0 + KM_BH && i0 < n; i0 += 32) {
+        const int64_t i = i0 + lane;
+        const bool in = i < n && i < b0 + KM_BH;
+        const int32_t a = in ? assign[i] : -1;
+        const unsigned act = __ballot_sync(0xffffffffu, in);
+        const unsigned peers = __match_any_sync(0xffffffffu, a) & act;
+        int32_t base = 0;
+        if (in) base = c[a];
+        __syncwarp();
+        if (in) {
+            const int32_t r = base + __popc(peers & lt);
+            order[start[a] + hist[b * k + a] + r] = (int32_t)i;
+            if ((peers & lt) == 0) c[a] = base + __popc(peers);  // group leader
+        }
+        __syncwarp();
+    }
+}
+
+// one warp per center: in-order sum of (c_j - p) over the center's segment
+template <class T, int KM_RMAX>
+__global__ void __launch_bounds__(256) km_segsum(const T *__restrict__ P, const T *__restrict__ C,
+                                                 const int32_t *__restrict__ order, const int32_t *__restrict__ start,
+                                                 int64_t k, int64_t d, const T *__restrict__ cost_bar,
+                                                 T *__restrict__ Cbar, T *__restrict__ H, int acc) {
+    const int lane = threadIdx.x & 31;
+    const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (j >= k) return;
+    const double ybar = (double)*cost_bar;
+    const int32_t s0 = start[j], s1 = start[j + 1];
+    const double two_y = 2.0 * ybar;
+    for (int64_t dc = 0; dc < d; dc += 32 * KM_RMAX) {
+        double cj[KM_RMAX], g[KM_RMAX];
+#pragma unroll
+        for (int r = 0; r < KM_RMAX; ++r) {
+            const int64_t t = dc + lane + 32 * r;
+            cj[r] = t < d ? (double)C[j * d + t] : 0.0;
+            g[r] = 0.0;
+        }
+        for (int32_t s = s0; s < s1; s += KM_SEGB) {
+            int32_t pi[KM_SEGB];
+#pragma unroll
+            for (int u = 0; u < KM_SEGB; ++u) pi[u] = (s + u < s1) ? __ldg(order + s + u) : -1;
+            double v[KM_SEGB][KM_RMAX];
+#pragma unroll
+            for (int u = 0; u < KM_SEGB; ++u)
+#pragma unroll
+                for (int r = 0; r < KM_RMAX; ++r) {
+                    const int64_t t = dc + lane + 32 * r;
+                    v[u][r] = (pi[u] >= 0 && t < d) ? (double)__ldg(P + (int64_t)pi[u] * d + t) : 0.0;
+                }
+#pragma unroll
+            for (int u = 0; u < KM_SEGB; ++u)
+                if (pi[u] >= 0) {
+#pragma unroll
+                    for (int r = 0; r < KM_RMAX; ++r) g[r] += cj[r] - v[u][r];
+                }
+        }
+        const double h = two_y * (double)(s1 - s0);
+#pragma unroll
+        for (int r = 0; r < KM_RMAX; ++r) {
+            const int64_t t = dc + lane + 32 * r;
+            if (t < d) {
+                const double cb = two_y * g[r];
+                Cbar[j * d + t] = acc ? (T)((double)Cbar[j * d + t] + cb) : (T)cb;
+                if (H) H[j * d + t] = acc ? (T)((double)H[j * d + t] + h) : (T)h;
+            }
+        }
+    }
+}
+
+template <class T>
+__global__ void km_cost_final(const double *__restrict__ part, int64_t np, T *__restrict__ cost, int acc) {
+    __shared__ double s[256];
+    double x = 0.0;
+    const int64_t per = (np + 255) / 256;
+    for (int64_t i = threadIdx.x * per; i < (threadIdx.x + 1) * per && i < np; ++i) x += part[i];
+    s[threadIdx.x] = x;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *cost = acc ? (T)((double)*cost + s[0]) : (T)s[0];
+}
+
+}  // namespace vjpk
+
+namespace {
+using namespace vjph;
+
+struct KmLayout {
+    size_t cn, part, hist, colsum, start, order, assign, total;
+    int64_t nbA, nbH;
+};
+KmLayout km_layout(int64_t n, int64_t k) {
+    KmLayout L{};
+    L.nbA = (n + vjpk::KM_BP - 1) / vjpk::KM_BP;
+    L.nbH = (n + vjpk::KM_BH - 1) / vjpk::KM_BH;
+    size_t off = 0;
+    L.cn = off; off += align256((size_t)k * 8);
+    L.part = off; off += align256((size_t)(L.nbA > 0 ? L.nbA : 1) * 8);
+    L.hist = off; off += align256((size_t)(L.nbH > 0 ? L.nbH : 1) * (size_t)k * 4);
+    L.colsum = off; off += align256((size_t)k * 4);
+    L.start = off; off += align256((size_t)(k + 1) * 4);
+    L.order = off; off += align256((size_t)(n > 0 ? n : 1) * 4);
+    L.assign = off; off += align256((size_t)(n > 0 ? n : 1) * 4);
+    L.total = off;
+    return L;
+}
+
+template <class T>
+vjp_status km_run(int64_t n, int64_t k, int64_t d, const void *P, const void *C, const void *cost_bar, void *Cbar,
+                  void *H, int32_t *assign, int64_t *counts, void *cost, void *ws, cudaStream_t s, unsigned flags) {
+    KmLayout L = km_layout(n, k);
+    unsigned char *w = static_cast<unsigned char *>(ws);
+    double *cn = reinterpret_cast<double *>(w + L.cn);
+    double *part = reinterpret_cast<double *>(w + L.part);
+    int32_t *hist = reinterpret_cast<int32_t *>(w + L.hist);
+    int32_t *colsum = reinterpret_cast<int32_t *>(w + L.colsum);
+    int32_t *start = reinterpret_cast<int32_t *>(w + L.start);
+    int32_t *order = reinterpret_cast<int32_t *>(w + L.order);
+    int32_t *asg = assign ? assign : reinterpret_cast<int32_t *>(w + L.assign);
+    const T *Pt = static_cast<const T *>(P);
+    const T *Ct = static_cast<const T *>(C);
+    const int acc = (flags & VJP_ACCUMULATE) ? 1 : 0;
+    int launches = 0;
+    vjpk::km_cnorm<T><<<(unsigned)((k + 127) / 128), 128, 0, s>>>(Ct, k, d, cn);
+    ++launches;
+    if (n > 0) {
+        const int64_t nd = (d + vjpk::KM_KD - 1) / vjpk::KM_KD;
+        const bool res = nd <= 2;
+        const size_t asm_ = ((size_t)(res ? nd * vjpk::KM_KD : 2 * vjpk::KM_KD) * vjpk::KM_BP +
+                             (size_t)2 * vjpk::KM_KD * vjpk::KM_BC) * 8;
+        auto ka = res ? vjpk::km_assign<T, true> : vjpk::km_assign<T, false>;
+        cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asm_);
+        ka<<<(unsigned)L.nbA, vjpk::KM_NT, asm_, s>>>(Pt, Ct, cn, n, k, d, asg, part);
+        const size_t hsm = (size_t)k * 4;
+        cudaFuncSetAttribute(vjpk::km_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
+        vjpk::km_hist<<<(unsigned)L.nbH, 256, hsm, s>>>(asg, n, k, hist);
+        launches += 2;
+    }
+    vjpk::km_colscan<<<(unsigned)((k + 127) / 128), 128, 0, s>>>(hist, n > 0 ? L.nbH : 0, k, colsum);
+    vjpk::km_startscan<<<1, 1024, 0, s>>>(colsum, k, start, counts, acc);
+    launches += 2;
+    if (n > 0) {
+        const int wpb = 4;
+        const size_t osm = (size_t)wpb * (size_t)k * 4;
+        cudaFuncSetAttribute(vjpk::km_order, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osm);
+        vjpk::km_order<<<(unsigned)((L.nbH + wpb - 1) / wpb), 32 * wpb, osm, s>>>(asg, n, k, hist, start, order,
+                                                                               L.nbH);
+        ++launches;
+    }
+    {
+        // dims per lane per pass: 32 R covers d = 32, 64 in one pass; wider d loops
+        auto ks = d <= 32 ? vjpk::km_segsum<T, 1> : (d <= 64 ? vjpk::km_segsum<T, 2> : vjpk::km_segsum<T, 4>);
+        ks<<<(unsigned)((k * 32 + 255) / 256), 256, 0, s>>>(Pt, Ct, order, start, k, d, static_cast<const T *>(cost_bar),
+                                                          static_cast<T *>(Cbar), static_cast<T *>(H), acc);
+    }
+    ++launches;
+    if (cost) {
+        if (n > 0) {
+            vjpk::km_cost_final<T><<<1, 256, 0, s>>>(part, L.nbA, static_cast<T *>(cost), acc);
+            ++launches;
+        } else if (!acc && cudaMemsetAsync(cost, 0, sizeof(T), s) != cudaSuccess) {
+            return VJP_ECUDA;
+        }
+    }
+    count_launch(launches);
+    return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+}
+
+constexpr int64_t kKmMaxK = 12288;  // per-block histograms and order counters live in shared memory
+}  // namespace
+
+extern "C" {
+
+size_t vjp_kmeans_workspace_bytes(vjp_dtype dtype, int64_t n, int64_t k, int64_t d) {
+    if ((dtype != VJP_F32 && dtype != VJP_F64) || n < 0 || k < 1 || d < 1) return 0;
+    return km_layout(n, k).total;
+}
+
+vjp_status vjp_kmeans(vjp_dtype dtype, int64_t n, int64_t k, int64_t d, const void *points, const void *centers,
+                      const void *cost_bar, void *centers_bar, void *hess_diag, int32_t *assign, int64_t *counts,
+                      void *cost, void *ws, size_t ws_bytes, vjp_stream_t stream, unsigned flags) {
+    if (dtype != VJP_F32 && dtype != VJP_F64) return VJP_EINVAL;
+    if (n < 0 || k < 1 || d < 1 || n >= ((int64_t)1 << 31) || k > kKmMaxK) return k > kKmMaxK ? VJP_EUNSUPPORTED : VJP_EINVAL;
+    if ((n > 0 && !points) || !centers || !cost_bar || !centers_bar) return VJP_EINVAL;
+    const size_t es = dtype == VJP_F64 ? 8 : 4;
+    const void *al[] = {points, centers, cost_bar, centers_bar, hess_diag, assign, counts, cost};
+    for (const void *p : al)
+        if (p && (reinterpret_cast<uintptr_t>(p) % es) != 0) return VJP_EALIGN;
+    if (ws_bytes < km_layout(n, k).total || !ws || !aligned16(ws)) return VJP_EWORKSPACE;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    return dtype == VJP_F64
+               ? km_run<double>(n, k, d, points, centers, cost_bar, centers_bar, hess_diag, assign, counts, cost, ws, s,
+                                flags)
+               : km_run<float>(n, k, d, points, centers, cost_bar, centers_bar, hess_diag, assign, counts, cost, ws, s,
+                               flags);
+}
+
+}  // extern "C"
