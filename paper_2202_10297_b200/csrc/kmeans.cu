@@ -25,6 +25,7 @@
 //                Hessian diagonal (jvp of the vjp, all-ones direction,
 //                P:1696-1700) H_j = 2 ybar cnt_j.
 #include <cstdint>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -34,7 +35,7 @@ constexpr int KM_BP = 128;   // points per assign CTA
 constexpr int KM_BC = 64;    // centers per tile
 constexpr int KM_KD = 32;    // dimensions per smem stage
 constexpr int KM_NT = 128;   // assign threads (16 x 8 grid of 8 x 8 tiles)
-constexpr int KM_BH = 4096;  // points per histogram block
+constexpr int KM_BH = 1024;  // points per histogram / ordering block
 constexpr int KM_SEGB = 16;  // rows gathered per batch in km_segsum
 
 // position of point pp (0..127) / center cc (0..63) in the swizzled smem rows:
@@ -232,6 +233,169 @@ __global__ void __launch_bounds__(KM_NT, 2) km_assign(const T *__restrict__ P, c
     if (t == 0) cost_part[blockIdx.x] = ((rv[0] + rv[1]) + rv[2]) + rv[3];
 }
 
+// ---------------------------------------------------------------------------
+// DMMA variant (mma.sync m8n8k4 f64, FP64 tensor cores): CTA = 128 points x
+// 64 centers, warp w = points [32w, 32w + 32) x 64 centers = 4 x 8 tiles of
+// 8 x 8; row-major smem tiles with a row stride = 4 (mod 16) doubles so the
+// A/B fragment loads (8 rows x 4 consecutive doubles) are conflict free.
+// Same candidate rule (||c||^2 - 2 p.c, first index on ties) as km_assign.
+constexpr int KM_PS_PAD = 4;
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+template <class T, bool RES>
+__global__ void __launch_bounds__(KM_NT, 2) km_assign_mma(const T *__restrict__ P, const T *__restrict__ C,
+                                                          const double *__restrict__ cn, int64_t n, int64_t k,
+                                                          int64_t d, int32_t *__restrict__ assign,
+                                                          double *__restrict__ cost_part) {
+    extern __shared__ __align__(16) double km_smem[];
+    const int nd = (int)((d + KM_KD - 1) / KM_KD);
+    const int PW = (RES ? nd * KM_KD : KM_KD) + KM_PS_PAD;  // P row stride (doubles)
+    constexpr int CW = KM_KD + KM_PS_PAD;                    // C row stride
+    double *Ps = km_smem;                                    // RES: [128][PW]; else [2][128][PW]
+    double *Cs = km_smem + (size_t)(RES ? 1 : 2) * KM_BP * PW;  // [2][64][CW]
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5, g = lane >> 2, tig = lane & 3;
+    const int64_t p0 = (int64_t)blockIdx.x * KM_BP;
+    const int nct = (int)((k + KM_BC - 1) / KM_BC), nst = nct * nd;
+
+    auto stage = [&](int st) {
+        const int ct = st / nd, dc = st % nd, buf = st & 1;
+        const int64_t c0 = (int64_t)ct * KM_BC, d0 = (int64_t)dc * KM_KD;
+        double *cs = Cs + (size_t)buf * KM_BC * CW;
+#pragma unroll 4
+        for (int idx = t; idx < KM_BC * KM_KD; idx += KM_NT) {
+            const int cc = idx / KM_KD, kk = idx % KM_KD;
+            const int64_t gc = c0 + cc, gd = d0 + kk;
+            const bool ok = gc < k && gd < d;
+            km_stage(cs + cc * CW + kk, C + (ok ? gc * d + gd : 0), ok);
+        }
+        if (!RES) {
+            double *ps = Ps + (size_t)buf * KM_BP * PW;
+#pragma unroll 4
+            for (int idx = t; idx < KM_BP * KM_KD; idx += KM_NT) {
+                const int pp = idx / KM_KD, kk = idx % KM_KD;
+                const int64_t gp = p0 + pp, gd = d0 + kk;
+                const bool ok = gp < n && gd < d;
+                km_stage(ps + pp * PW + kk, P + (ok ? gp * d + gd : 0), ok);
+            }
+        }
+        km_commit();
+    };
+    if (RES) {
+        const int DP = nd * KM_KD;
+#pragma unroll 4
+        for (int idx = t; idx < KM_BP * DP; idx += KM_NT) {
+            const int pp = idx / DP, kk = idx % DP;
+            const int64_t gp = p0 + pp;
+            const bool ok = gp < n && kk < d;
+            km_stage(Ps + pp * PW + kk, P + (ok ? gp * d + kk : 0), ok);
+        }
+    }
+    stage(0);
+
+    double bv[4];
+    int32_t bj[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        bv[i] = INFINITY;
+        bj[i] = 0x7fffffff;
+    }
+    double pnorm = 0.0;
+    double acc[4][8][2];
+    for (int st = 0; st < nst; ++st) {
+        const int ct = st / nd, dc = st % nd;
+        if (dc == 0) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        }
+        if (st + 1 < nst) {
+            __syncthreads();
+            stage(st + 1);
+            km_wait<1>();
+        } else {
+            km_wait<0>();
+        }
+        __syncthreads();
+        const double *ps = RES ? Ps + dc * KM_KD : Ps + (size_t)(st & 1) * KM_BP * PW;
+        const double *cs = Cs + (size_t)(st & 1) * KM_BC * CW;
+        if (ct == 0) {
+#pragma unroll 8
+            for (int kk = 0; kk < KM_KD; ++kk) {
+                const double v = ps[t * PW + kk];
+                pnorm = fma(v, v, pnorm);
+            }
+        }
+#pragma unroll 2
+        for (int k4 = 0; k4 < KM_KD; k4 += 4) {
+            double a[4], b[8];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) a[mi] = ps[(w * 32 + mi * 8 + g) * PW + k4 + tig];
+#pragma unroll
+            for (int ni = 0; ni < 8; ++ni) b[ni] = cs[(ni * 8 + g) * CW + k4 + tig];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+                for (int ni = 0; ni < 8; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        }
+        if (dc == nd - 1) {
+            const int64_t c0 = (int64_t)ct * KM_BC;
+#pragma unroll
+            for (int ni = 0; ni < 8; ++ni)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int64_t gc = c0 + ni * 8 + tig * 2 + e;
+                    if (gc < k) {
+                        const double cnj = cn[gc];
+#pragma unroll
+                        for (int mi = 0; mi < 4; ++mi) {
+                            const double v = fma(-2.0, acc[mi][ni][e], cnj);
+                            if (v < bv[mi] || (v == bv[mi] && (int32_t)gc < bj[mi])) {
+                                bv[mi] = v;
+                                bj[mi] = (int32_t)gc;
+                            }
+                        }
+                    }
+                }
+        }
+    }
+    // the 4 threads of a group share their points: combine (first index on ties)
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int o = 1; o < 4; o <<= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, bv[mi], o);
+            const int32_t oj = __shfl_xor_sync(0xffffffffu, bj[mi], o);
+            if (ov < bv[mi] || (ov == bv[mi] && oj < bj[mi])) {
+                bv[mi] = ov;
+                bj[mi] = oj;
+            }
+        }
+    __syncthreads();
+    double *pn = Cs;          // [128] ||p||^2
+    double *mv = Cs + KM_BP;  // [128] min candidate
+    pn[t] = pnorm;
+    if (tig == 0) {
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+            const int pp = w * 32 + mi * 8 + g;
+            mv[pp] = bv[mi];
+            const int64_t gp = p0 + pp;
+            if (gp < n) assign[gp] = bj[mi];
+        }
+    }
+    __syncthreads();
+    double md = (p0 + t < n) ? fmax(pn[t] + mv[t], 0.0) : 0.0;
+    for (int o = 16; o > 0; o >>= 1) md += __shfl_down_sync(0xffffffffu, md, o);
+    __syncthreads();
+    if (lane == 0) mv[w] = md;
+    __syncthreads();
+    if (t == 0) cost_part[blockIdx.x] = ((mv[0] + mv[1]) + mv[2]) + mv[3];
+}
+
 __global__ void km_hist(const int32_t *__restrict__ assign, int64_t n, int64_t k, int32_t *__restrict__ hist) {
     extern __shared__ int32_t h[];
     for (int64_t j = threadIdx.x; j < k; j += blockDim.x) h[j] = 0;
@@ -242,17 +406,40 @@ __global__ void km_hist(const int32_t *__restrict__ assign, int64_t n, int64_t k
     for (int64_t j = threadIdx.x; j < k; j += blockDim.x) hist[(int64_t)blockIdx.x * k + j] = h[j];
 }
 
-// per center (column): exclusive scan over the blocks in place, column total
-__global__ void km_colscan(int32_t *__restrict__ hist, int64_t nb, int64_t k, int32_t *__restrict__ colsum) {
-    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= k) return;
+// per center (column): exclusive scan over the blocks in place, column total.
+// CTA = 32 centers (x, coalesced) x 32 block segments (y): segment sums, a
+// scan of the 32 segment sums in shared memory, then the in-place rewrite.
+__global__ void __launch_bounds__(1024) km_colscan(int32_t *__restrict__ hist, int64_t nb, int64_t k,
+                                                   int32_t *__restrict__ colsum) {
+    __shared__ int32_t seg[32][33];
+    const int x = threadIdx.x & 31, y = threadIdx.x >> 5;
+    const int64_t j = (int64_t)blockIdx.x * 32 + x;
+    const int64_t per = (nb + 31) / 32, b0 = y * per, b1 = b0 + per < nb ? b0 + per : nb;
     int32_t s = 0;
-    for (int64_t b = 0; b < nb; ++b) {
-        const int32_t v = hist[b * k + j];
-        hist[b * k + j] = s;
-        s += v;
+    if (j < k) {
+#pragma unroll 8
+        for (int64_t b = b0; b < b1; ++b) s += hist[b * k + j];
     }
-    colsum[j] = s;
+    seg[y][x] = s;
+    __syncthreads();
+    if (y == 0) {
+        int32_t run = 0;
+        for (int q = 0; q < 32; ++q) {
+            const int32_t v = seg[q][x];
+            seg[q][x] = run;
+            run += v;
+        }
+        if (j < k) colsum[j] = run;
+    }
+    __syncthreads();
+    if (j < k) {
+        int32_t run = seg[y][x];
+        for (int64_t b = b0; b < b1; ++b) {
+            const int32_t v = hist[b * k + j];
+            hist[b * k + j] = run;
+            run += v;
+        }
+    }
 }
 
 // exclusive scan of the column totals (one CTA of 1024 threads): start[j], start[k] = n
@@ -307,10 +494,13 @@ __global__ void km_order(const int32_t *__restrict__ assign, int64_t n, int64_t 
     if (b >= nb) return;
     const int64_t b0 = b * KM_BH;
     const unsigned lt = (1u << lane) - 1u;
-    for (int64_t i0 = b0; i0 < b0 + KM_BH && i0 < n; i0 += 32) {
+    const int64_t b1 = b0 + KM_BH < n ? b0 + KM_BH : n;
+    int32_t an = (b0 + lane < b1) ? __ldg(assign + b0 + lane) : -1;
+    for (int64_t i0 = b0; i0 < b1; i0 += 32) {
         const int64_t i = i0 + lane;
-        const bool in = i < n && i < b0 + KM_BH;
-        const int32_t a = in ? assign[i] : -1;
+        const bool in = i < b1;
+        const int32_t a = an;
+        an = (i + 32 < b1) ? __ldg(assign + i + 32) : -1;  // next round in flight
         const unsigned act = __ballot_sync(0xffffffffu, in);
         const unsigned peers = __match_any_sync(0xffffffffu, a) & act;
         int32_t base = 0;
@@ -440,15 +630,28 @@ vjp_status km_run(int64_t n, int64_t k, int64_t d, const void *P, const void *C,
         const bool res = nd <= 2;
         const size_t asm_ = ((size_t)(res ? nd * vjpk::KM_KD : 2 * vjpk::KM_KD) * vjpk::KM_BP +
                              (size_t)2 * vjpk::KM_KD * vjpk::KM_BC) * 8;
-        auto ka = res ? vjpk::km_assign<T, true> : vjpk::km_assign<T, false>;
-        cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asm_);
-        ka<<<(unsigned)L.nbA, vjpk::KM_NT, asm_, s>>>(Pt, Ct, cn, n, k, d, asg, part);
+        static const int use_mma = [] {
+            const char *e = std::getenv("VJP_KMEANS_FFMA");
+            return (e && *e == '1') ? 0 : 1;
+        }();
+        if (use_mma) {
+            const int PW = (res ? (int)nd * vjpk::KM_KD : vjpk::KM_KD) + vjpk::KM_PS_PAD;
+            const size_t msm = ((size_t)(res ? 1 : 2) * vjpk::KM_BP * PW +
+                                (size_t)2 * vjpk::KM_BC * (vjpk::KM_KD + vjpk::KM_PS_PAD)) * 8;
+            auto km = res ? vjpk::km_assign_mma<T, true> : vjpk::km_assign_mma<T, false>;
+            cudaFuncSetAttribute(km, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm);
+            km<<<(unsigned)L.nbA, vjpk::KM_NT, msm, s>>>(Pt, Ct, cn, n, k, d, asg, part);
+        } else {
+            auto ka = res ? vjpk::km_assign<T, true> : vjpk::km_assign<T, false>;
+            cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asm_);
+            ka<<<(unsigned)L.nbA, vjpk::KM_NT, asm_, s>>>(Pt, Ct, cn, n, k, d, asg, part);
+        }
         const size_t hsm = (size_t)k * 4;
         cudaFuncSetAttribute(vjpk::km_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
         vjpk::km_hist<<<(unsigned)L.nbH, 256, hsm, s>>>(asg, n, k, hist);
         launches += 2;
     }
-    vjpk::km_colscan<<<(unsigned)((k + 127) / 128), 128, 0, s>>>(hist, n > 0 ? L.nbH : 0, k, colsum);
+    vjpk::km_colscan<<<(unsigned)((k + 31) / 32), 1024, 0, s>>>(hist, n > 0 ? L.nbH : 0, k, colsum);
     vjpk::km_startscan<<<1, 1024, 0, s>>>(colsum, k, start, counts, acc);
     launches += 2;
     if (n > 0) {
