@@ -47,33 +47,79 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region: NVML
+    (in-process, every 2 ms, so even a ~50 ms region gets many samples), else
+    an nvidia-smi -lms subprocess started (and waited for) before the region."""
 
+    NAMES = {"hw_slowdown": "HwSlowdown", "hw_thermal_slowdown": "HwThermalSlowdown",
+             "sw_thermal_slowdown": "SwThermalSlowdown", "sw_power_cap": "SwPowerCap",
+             "hw_power_brake_slowdown": "HwPowerBrakeSlowdown"}
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
-        self.rows = []
+        self.rows = []  # (sm_mhz, max_mhz, set of reason names)
         self.proc = None
+        self.nvml = None
+        self.stop = threading.Event()
+        self.src = None
 
     def __enter__(self):
         try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            self.nvml = (pynvml, h)
+            self.src = "nvml"
+            self.t = threading.Thread(target=self._nvml_loop, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
+        try:
+            self.src = "nvidia-smi"
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._smi_read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 10:  # first sample before the region starts
+                time.sleep(0.01)
+            self.rows.clear()
         except Exception:
             self.proc = None
         return self
 
-    def _read(self):
+    def _nvml_loop(self):
+        pynvml, h = self.nvml
+        while not self.stop.is_set():
+            try:
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+                r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                act = {k for k, v in self.NAMES.items() if r & getattr(pynvml, "nvmlClocksEventReason" + v, 0)}
+                self.rows.append((float(sm), float(mx), act))
+            except Exception:
+                pass
+            self.stop.wait(0.002)
+
+    def _smi_read(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            r = [x.strip() for x in line.split(",")]
+            try:
+                act = {names[i] for i in range(4) if len(r) > 3 + i and r[3 + i].lower().startswith("active")}
+                self.rows.append((float(r[0]), float(r[1]), act))
+            except ValueError:
+                pass
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nvml:
+            self.t.join(timeout=1)
         if self.proc:
             self.proc.terminate()
             try:
@@ -83,14 +129,11 @@ class ClockSampler:
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 3 + i and r[3 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock samples"], "source": self.src}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted(set().union(*[r[2] for r in self.rows]))
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": reasons, "samples": len(self.rows), "source": self.src}
 
 
 def dist_env():
@@ -340,6 +383,14 @@ def run_extra(args):
                 o = torch.empty(N28, dtype=torch.float64, device=dev)
                 cases.append((f"rbi {op.upper()} f64 n=2^28 m={m}", N28, nb * N28,
                               (lambda op=op, inds=inds, a=a, hb=hb, o=o: vjp.reduce_by_index(op, inds, a, hb, out=o))))
+    if w in ("kmeans", "all"):
+        # config 5: n = 10^6 points, d = 64, k = 1024, f64 (one call: forward
+        # distance/argmin on the FP64 tensor pipe + the return sweep)
+        nk, kk, dk = 1_000_000, 1024, 64
+        P, C = synth.kmeans_inputs(nk, kk, dk, device=dev)
+        out = vjp.kmeans(P, C, 1.0)
+        cases.append((f"kmeans grad n=1e6 k=1024 d=64 f64 (flops {2 * nk * kk * dk:.3g})", nk,
+                      nk * dk * 8 * 2, lambda P=P, C=C, out=out: vjp.kmeans(P, C, 1.0, out=out)))
     for name, n, nbytes, fn in cases:
         for _ in range(args.warmup):
             fn()
@@ -370,7 +421,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", default="config2",
-                    choices=["config2", "scan_add", "scan_linrec30", "reduce", "rbi", "all"],
+                    choices=["config2", "scan_add", "scan_linrec30", "reduce", "rbi", "kmeans", "all"],
                     help="config2 = the headline line; the others print per-call extra lines")
     args = ap.parse_args()
     if args.warmup < 3:

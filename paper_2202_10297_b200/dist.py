@@ -12,6 +12,10 @@ exchange step:
   reduce_by_index per-bin state -> all_reduce (PRODUCT+SUM for *, MAX/MIN then
                   MIN of candidate indices for max/min) -> finish; ADD needs no
                   exchange (hs_bar is replicated).
+  kmeans          (config 5) points partitioned by rank, centers replicated:
+                  every output is a sum over points, so the per-rank partials
+                  (centers_bar, Hessian diagonal, counts, cost) are all_reduced
+                  (SUM, k*d*8 B twice + k*8 B).
 
 All arithmetic runs in libvjp_b200.so; this module only sequences the calls and
 the collectives on the current stream.
@@ -156,3 +160,19 @@ def reduce_by_index(op, inds: torch.Tensor, as_: torch.Tensor | None, hs_bar: to
                                         _p(bin_aux), _p(ws), nbytes, sh, s, ACCUMULATE if accumulate else 0),
            "vjp_reduce_by_index_finish")
     return ab
+
+
+def kmeans(points: torch.Tensor, centers: torch.Tensor, cost_bar=1.0, *, group=None, hess: bool = True):
+    """config 5 over the ranks: this rank's points (any contiguous slice of the
+    global point set), replicated centers; returns the GLOBAL cbar / hdiag /
+    counts / cost (all_reduce SUM of the per-rank partials) and this rank's
+    assignment."""
+    from . import kmeans as _kmeans
+    r = _kmeans(points, centers, cost_bar, hess=hess)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        for key in ("cbar", "hdiag", "counts"):
+            if r[key] is not None:
+                _all_reduce(r[key], dist.ReduceOp.SUM, group)
+        c = r["cost"].reshape(1)
+        _all_reduce(c, dist.ReduceOp.SUM, group)
+    return r

@@ -85,6 +85,20 @@ def _worker(rank, world, port, q):
             if rank == 0:
                 ref = oracle.vjp_reduce_by_index(op, inds.numpy(), a.numpy(), hb.numpy())[0]
                 assert_close(np.concatenate(parts), ref, np.float64, what=f"2-rank rbi {op}")
+        # config-5 k-means gradient: points split by rank, all_reduce of partials
+        N, K, D = 40_003, 96, 24
+        P, C = synth.kmeans_inputs(N, K, D)
+        off, n = vdist.shard_bounds(N, world, rank)
+        r = vdist.kmeans(P[off:off + n].to(dev), C.to(dev), 0.5)
+        if rank == 0:
+            ref = oracle.kmeans(P.numpy(), C.numpy(), cost_bar=0.5)
+            assert np.array_equal(r["counts"].cpu().numpy(), ref["counts"])
+            assert np.array_equal(r["hdiag"].cpu().numpy(), ref["hdiag"])
+            a = ref["assign"]
+            scale = np.zeros((K, D))
+            np.add.at(scale, a, np.abs(C.numpy()[a] - P.numpy()))  # condition scaling (reading A22)
+            assert_close(r["cbar"].cpu().numpy().ravel(), ref["cbar"].ravel(), np.float64,
+                         scale=(2 * 0.5 * scale).ravel(), what="2-rank kmeans")
         dist.barrier()
         dist.destroy_process_group()
         q.put((rank, "ok"))
