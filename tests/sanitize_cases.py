@@ -16,6 +16,9 @@ for op in ('add', 'mul', 'min', 'max', 'linrec', 'mat2'):
         if a is not None:
             vjp.scan(op, yb, a, want_ys=True)
         vjp.scan(op, yb, a, out=torch.zeros_like(yb), accumulate=True)
+        if op in ('add', 'mul', 'linrec', 'mat2'):  # the opt-in one-read sweep (producer / carry warps)
+            vjp.scan(op, yb, a, sweep=True)
+            vjp.scan(op, yb, a, out=torch.zeros_like(yb), accumulate=True, sweep=True)
 for op in ('add', 'mul', 'min', 'max'):
     for n in (1, 999, 100_003):
         a = synth.mul_inputs(n, zeros='one', dtype=torch.float64, device=dev)
@@ -28,5 +31,9 @@ for op in ('add', 'mul', 'min', 'max'):
 is_, yb = synth.scatter_inputs(10_000, 3000, device=dev)
 vjp.scatter(is_, yb)
 vjp.scatter(is_, yb.clone(), in_place=True)
+for n, k, d in ((1, 1, 1), (129, 65, 17), (5000, 100, 64), (3000, 20, 70)):  # config-5 composite
+    for dt in (torch.float64, torch.float32):
+        P, C = synth.kmeans_inputs(n, k, d, dtype=dt, device=dev)
+        vjp.kmeans(P, C, 1.0)
 torch.cuda.synchronize()
 print('sanitize cases done')
