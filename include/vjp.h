@@ -292,6 +292,25 @@ vjp_status vjp_scatter(vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, i
                        size_t ws_bytes, vjp_stream_t stream, unsigned flags);
 
 /* ======================================================================
+ * vjp_scan_batched — vjp of a VECTORISED scan
+ *
+ * ys = scan (map (.)) e xs over n elements of `width` components each; the
+ * paper's transpose rule makes it `width` independent scans
+ * along n, component j of element i at [i][j] (each component Op::W scalars:
+ * 1 for ADD/MUL, (d, c) for LINREC, a row-major 2x2 for MAT2).  The return
+ * sweep is computed per component exactly as vjp_scan (the vectorised plus
+ * case, is the per-column reversed suffix sum).
+ *   as [n][width][W] (NULL allowed for ADD); ys_bar, as_bar likewise.
+ * VJP_ACCUMULATE: as_bar += .  MIN/MAX -> VJP_EUNSUPPORTED (their reverse maps
+ * need the forward carry; use vjp_scan per component).  Errors: VJP_EINVAL,
+ * VJP_EALIGN, VJP_EWORKSPACE, VJP_ECUDA.
+ * ==================================================================== */
+size_t vjp_scan_batched_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_t n, int64_t width);
+vjp_status vjp_scan_batched(vjp_op op, vjp_dtype dtype, int64_t n, int64_t width, const void *as,
+                            const void *ys_bar, void *as_bar, void *ws, size_t ws_bytes,
+                            vjp_stream_t stream, unsigned flags);
+
+/* ======================================================================
  * vjp_kmeans — composite k-means cost gradient (BASELINE
  * config 5)
  *

@@ -193,3 +193,20 @@ def kmeans(points: np.ndarray, centers: np.ndarray, cost_bar: float = 1.0):
     if rc != 0:
         raise RuntimeError(f"oracle_kmeans rc={rc}")
     return {"cost": float(cost[0]), "cbar": cbar, "hdiag": hdiag, "assign": assign, "counts": counts}
+
+
+def vjp_scan_batched(op, ys_bar: np.ndarray, as_: np.ndarray | None, width: int, *, out=None,
+                     accumulate: bool = False):
+    """vjp of the VECTORISED scan ys = scan (map op) e as_ by the
+    paper's transpose rule: `width` independent scans along n,
+    each by the sequential oracle_vjp_scan.  Arrays hold [n][width][W] scalars."""
+    W = WIDTH[_op(op)]
+    yb = np.ascontiguousarray(ys_bar).reshape(-1, width, W)
+    a = None if as_ is None else np.ascontiguousarray(as_).reshape(-1, width, W)
+    res = np.empty_like(yb) if out is None else np.ascontiguousarray(out).reshape(-1, width, W).copy()
+    for j in range(width):  # transpose |> map (scan op e) |> transpose
+        col_out = res[:, j, :].reshape(-1).copy()
+        r = vjp_scan(op, yb[:, j, :].reshape(-1).copy(), None if a is None else a[:, j, :].reshape(-1).copy(),
+                     out=col_out if accumulate else None, accumulate=accumulate)
+        res[:, j, :] = np.asarray(r).reshape(-1, W)
+    return res.reshape(-1)

@@ -79,6 +79,8 @@ def lib():
             "vjp_scatter_workspace_bytes": ([ci, i64, i64], sz),
             "vjp_scatter": ([ci, ci, i64, i64, i64, vp, vp, vp, vp, vp, sz, vp, u32], ci),
             "vjp_kmeans_workspace_bytes": ([ci, i64, i64, i64], sz),
+            "vjp_scan_batched_workspace_bytes": ([ci, ci, i64, i64], sz),
+            "vjp_scan_batched": ([ci, ci, i64, i64, vp, vp, vp, vp, sz, vp, u32], ci),
             "vjp_kmeans": ([ci, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, u32], ci),
         }
         for name, (args, res) in sig.items():
@@ -355,3 +357,31 @@ def kmeans(points: torch.Tensor, centers: torch.Tensor, cost_bar=1.0, *, hess: b
                         _p(ws), 0 if ws is None else ws.numel(), _stream(dev), ACCUMULATE if accumulate else 0),
            "vjp_kmeans")
     return {"cbar": cbar, "hdiag": hd, "assign": asg, "counts": cnt, "cost": cost}
+
+
+def scan_batched(op, ys_bar: torch.Tensor, as_: torch.Tensor | None = None, *, width: int,
+                 out: torch.Tensor | None = None, accumulate: bool = False):
+    """as_bar of the VECTORISED scan ys = scan (map op) e as_:
+    `width` independent scans along the leading dimension, element i component
+    j at [i][j] (op width W scalars each).  Tensors hold n * width * W scalars."""
+    o = _op(op)
+    host = not ys_bar.is_cuda
+    dev = _dev_of(ys_bar, as_, out)
+    yb = _to(ys_bar, dev)
+    a = _to(as_, dev)
+    w = WIDTH[o]
+    if yb.numel() % (w * width):
+        raise ValueError(f"ys_bar has {yb.numel()} scalars, not a multiple of width*{w}")
+    n = yb.numel() // (w * width)
+    if a is not None and (a.numel() != yb.numel() or a.dtype != yb.dtype):
+        raise ValueError("as_ must match ys_bar in size and dtype")
+    ab = _out_buf(out, yb, dev, accumulate)
+    L = lib()
+    ws = workspace(L.vjp_scan_batched_workspace_bytes(o, _dt(yb), n, width), dev)
+    _check(L.vjp_scan_batched(o, _dt(yb), n, width, _p(a), _p(yb), _p(ab), _p(ws), 0 if ws is None else ws.numel(),
+                              _stream(dev), ACCUMULATE if accumulate else 0), "vjp_scan_batched")
+    if out is not None and not out.is_cuda:
+        out.copy_(ab, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        return out
+    return _host_out(ab, host)
