@@ -291,6 +291,10 @@ vjp_status vjp_scatter(vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, i
                        const void *is, const void *ys_bar, void *xs_bar, void *vs_bar, void *ws,
                        size_t ws_bytes, vjp_stream_t stream, unsigned flags);
 
+/* Test hook: y[i] = log2|x[i]| (DEVICE arrays, f64) by the routine the MUL
+ * histograms accumulate with (reduce_by_index log domain). */
+vjp_status vjp_debug_log2_abs(const double *x, double *y, int64_t n, vjp_stream_t stream);
+
 /* ======================================================================
  * vjp_scan_batched — vjp of a VECTORISED scan
  *

@@ -80,6 +80,7 @@ def lib():
             "vjp_scatter": ([ci, ci, i64, i64, i64, vp, vp, vp, vp, vp, sz, vp, u32], ci),
             "vjp_kmeans_workspace_bytes": ([ci, i64, i64, i64], sz),
             "vjp_scan_batched_workspace_bytes": ([ci, ci, i64, i64], sz),
+            "vjp_debug_log2_abs": ([vp, vp, i64, vp], ci),
             "vjp_scan_batched": ([ci, ci, i64, i64, vp, vp, vp, vp, sz, vp, u32], ci),
             "vjp_kmeans": ([ci, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, u32], ci),
         }

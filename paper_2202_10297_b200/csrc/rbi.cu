@@ -210,6 +210,52 @@ __device__ __forceinline__ void rbi_stream(const I *__restrict__ inds, const T *
     }
 }
 
+// log2|x| for finite x != 0 (the MUL histograms' log domain), without the
+// library routine's special-case paths: x = m * 2^e with m in [sqrt(1/2),
+// sqrt(2)), ln m = 2 atanh(s), s = (m - 1)/(m + 1) (|s| <= 0.1716; m - 1 is
+// exact by Sterbenz), atanh(s)/s = sum_k s^(2k)/(2k+1) to k = 11 (truncation
+// < 1e-18).  Error: a few ulp of log2 m plus one rounding of e + log2 m —
+// the same order as log2() (measured against log2() in
+// tests/test_gpu_rbi.py::test_rbi_mul_log2_accuracy).  Denormals are rescaled.
+__device__ __forceinline__ double log2_abs(double x) {
+    long long b = __double_as_longlong(x) & 0x7fffffffffffffffll;
+    int e = (int)(b >> 52);
+    if (e == 0) {  // subnormal
+        b = __double_as_longlong(__longlong_as_double(b) * 0x1p54);
+        e = (int)(b >> 52) - 54;
+    }
+    e -= 1023;
+    double m = __longlong_as_double((b & 0x000fffffffffffffll) | 0x3ff0000000000000ll);
+    if (m > 1.4142135623730951) {
+        m *= 0.5;
+        e += 1;
+    }
+    const double s = (m - 1.0) / (m + 1.0);
+    const double s2 = s * s;
+    double p = 1.0 / 23.0;
+    p = fma(p, s2, 1.0 / 21.0);
+    p = fma(p, s2, 1.0 / 19.0);
+    p = fma(p, s2, 1.0 / 17.0);
+    p = fma(p, s2, 1.0 / 15.0);
+    p = fma(p, s2, 1.0 / 13.0);
+    p = fma(p, s2, 1.0 / 11.0);
+    p = fma(p, s2, 1.0 / 9.0);
+    p = fma(p, s2, 1.0 / 7.0);
+    p = fma(p, s2, 1.0 / 5.0);
+    p = fma(p, s2, 1.0 / 3.0);
+    const double t = s * s2 * p;  // atanh(s) - s
+    // log2 m = 2 (s + t) / ln 2, with 2/ln 2 split hi + lo for the dominant term
+    const double k_hi = 2.8853900817779268, k_lo = 4.0710547481862066e-17;
+    const double l = fma(s, k_hi, fma(s, k_lo, t * k_hi));
+    return (double)e + l;
+}
+
+// test hook: log2_abs on n values (tests compare it with log2 on the device)
+__global__ void rbi_log2_probe(const double *x, double *y, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) y[i] = log2_abs(x[i]);
+}
+
 // MUL, large m: every element must contribute, and a CAS-multiply costs two
 // dependent L2 round trips per element.  Instead accumulate log2|a| with
 // fire-and-forget f64 red.add, count zeros and negative factors, and finalise
@@ -225,7 +271,7 @@ __global__ void __launch_bounds__(kBThreads) rbi_fwd_log(const I *__restrict__ i
         if (x == 0.0) {
             atomicAdd(P.z + b, 1ull);
         } else {
-            atomicAdd(P.p + b, log2(fabs(x)));
+            atomicAdd(P.p + b, log2_abs(x));
             if (x < 0.0) atomicAdd(P.ng + b, 1ull);
         }
     });
@@ -249,7 +295,7 @@ __global__ void __launch_bounds__(kBThreads) rbi_fwd_smem_log(const I *__restric
         if (x == 0.0) {
             atomicAdd(zc + b, 1u);
         } else {
-            atomicAdd(lg + b, log2(fabs(x)));
+            atomicAdd(lg + b, log2_abs(x));
             if (x < 0.0) atomicAdd(nc + b, 1u);
         }
     });
@@ -756,6 +802,16 @@ vjp_status common_check(vjp_op op, vjp_dtype dtype, vjp_itype itype, int64_t n, 
 }  // namespace
 
 extern "C" {
+
+// test hook for the MUL log domain: y[i] = log2|x[i]| by the kernels' routine
+vjp_status vjp_debug_log2_abs(const double *x, double *y, int64_t n, vjp_stream_t stream) {
+    if (n < 0 || (n > 0 && (!x || !y))) return VJP_EINVAL;
+    if (n == 0) return VJP_OK;
+    vjpk::rbi_log2_probe<<<(unsigned)((n + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(x, y, n);
+    vjph::count_launch();
+    return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+}
+
 
 size_t vjp_reduce_by_index_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_t n, int64_t m) {
     (void)dtype;
