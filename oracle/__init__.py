@@ -108,21 +108,25 @@ def vjp_scan(op, ys_bar: np.ndarray, as_: np.ndarray | None = None, *, out=None,
     return (as_bar, ys) if want_ys else as_bar
 
 
-def vjp_reduce(op, as_: np.ndarray, y_bar: float, *, out=None, accumulate: bool = False):
-    """Returns (as_bar, y, arg, zeros) for y = reduce op as_."""
+def vjp_reduce(op, as_: np.ndarray, y_bar, *, out=None, accumulate: bool = False):
+    """Returns (as_bar, y, arg, zeros) for y = reduce op as_.
+    LINREC / MAT2 (the general rule): as_ holds n elements of W
+    scalars, y_bar and y are W-vectors."""
     o = _op(op)
+    w = WIDTH[o]
     as_ = np.ascontiguousarray(as_)
     dt = _dt(as_)
-    yb = np.array([y_bar], dtype=as_.dtype)
-    y = np.zeros(1, dtype=as_.dtype)
+    yb = np.ascontiguousarray(np.asarray(y_bar, dtype=as_.dtype).reshape(-1))
+    assert yb.size == w
+    y = np.zeros(w, dtype=as_.dtype)
     arg = np.zeros(1, dtype=np.int64)
     zeros = np.zeros(1, dtype=np.int64)
     as_bar = np.zeros_like(as_) if out is None else out
-    rc = lib().oracle_vjp_reduce(o, dt, as_.size, _p(as_), _p(yb), _p(as_bar), _p(y), _p(arg),
+    rc = lib().oracle_vjp_reduce(o, dt, as_.size // w, _p(as_), _p(yb), _p(as_bar), _p(y), _p(arg),
                                  _p(zeros), ACCUMULATE if accumulate else 0)
     if rc != 0:
         raise RuntimeError(f"oracle_vjp_reduce rc={rc}")
-    return as_bar, y[0], int(arg[0]), int(zeros[0])
+    return as_bar, (y[0] if w == 1 else y), int(arg[0]), int(zeros[0])
 
 
 def vjp_reduce_by_index(op, inds: np.ndarray, as_: np.ndarray | None, hs_bar: np.ndarray, *,

@@ -239,9 +239,64 @@ int oracle_vjp_scan(int op, int dtype, int64_t n, const void *as, const void *ys
  *              writes 0 everywhere else; ACCUMULATE touches only i_y.
  * y_bar is a host pointer to one element of dtype; y (nullable) receives y.
  */
+/*
+ * The paper's GENERAL reduce rule for an operator with no
+ * special case (here the d-vector operators LINREC and MAT2):
+ *     ls = scan^exc (.) e as
+ *     rs = reverse as |> scan^exc (\x y -> y (.) x) e |> reverse     (A18)
+ *     asbar_i += d(l_i (.) a_i (.) r_i)/da_i . ybar
+ * The last line is Eq. 3 applied to v = x (.) r_i with x = l_i (.) a_i:
+ * xbar = dv/dx^T ybar, then abar = d(l_i (.) a_i)/da_i^T xbar (op_vjp twice).
+ * y_bar holds one element (W scalars); y receives the reduction.
+ */
+static int reduce_general(int op, int dtype, int64_t n, const void *as, const void *y_bar, void *as_bar,
+                          void *y, int64_t *arg, int64_t *zeros, unsigned flags) {
+    const int W = width_of(op);
+    if (!y_bar || (n > 0 && (!as || !as_bar))) return O_EINVAL;
+    LD ybar[4], e[4];
+    for (int k = 0; k < W; ++k) ybar[k] = ld_get(dtype, y_bar, k);
+    /* neutral element: LINREC (0, 1), MAT2 I */
+    if (op == O_LINREC) { e[0] = 0.0L; e[1] = 1.0L; }
+    else { e[0] = 1.0L; e[1] = 0.0L; e[2] = 0.0L; e[3] = 1.0L; }
+    LD *ls = (LD *)malloc(sizeof(LD) * (size_t)(n > 0 ? n : 1) * W);
+    LD *rs = (LD *)malloc(sizeof(LD) * (size_t)(n > 0 ? n : 1) * W);
+    if (!ls || !rs) { free(ls); free(rs); return O_EINVAL; }
+    LD acc[4], a[4], t[4];
+    for (int k = 0; k < W; ++k) acc[k] = e[k];
+    for (int64_t i = 0; i < n; ++i) {   /* ls: exclusive forward scan */
+        for (int k = 0; k < W; ++k) { ls[i * W + k] = acc[k]; a[k] = ld_get(dtype, as, i * W + k); }
+        op_apply(op, acc, a, t);
+        for (int k = 0; k < W; ++k) acc[k] = t[k];
+    }
+    if (y) for (int k = 0; k < W; ++k) ld_put(dtype, y, k, acc[k], 0);
+    for (int k = 0; k < W; ++k) acc[k] = e[k];
+    for (int64_t i = n - 1; i >= 0; --i) {  /* rs: exclusive scan of the reversed array, flipped (.) */
+        for (int k = 0; k < W; ++k) { rs[i * W + k] = acc[k]; a[k] = ld_get(dtype, as, i * W + k); }
+        op_apply(op, a, acc, t);  /* (\x y -> y (.) x) acc a = a (.) acc */
+        for (int k = 0; k < W; ++k) acc[k] = t[k];
+    }
+    for (int64_t i = 0; i < n; ++i) {
+        LD x[4], xbar[4], gr_unused[4], ga[4], ga_r[4];
+        for (int k = 0; k < W; ++k) a[k] = ld_get(dtype, as, i * W + k);
+        op_apply(op, ls + i * W, a, x);                     /* x = l_i (.) a_i */
+        for (int k = 0; k < W; ++k) xbar[k] = 0.0L;
+        op_vjp(op, x, rs + i * W, ybar, ga_r, xbar);        /* xbar = d(x (.) r_i)/dx^T ybar */
+        for (int k = 0; k < W; ++k) gr_unused[k] = 0.0L;
+        op_vjp(op, ls + i * W, a, xbar, ga, gr_unused);     /* abar_i = d(l_i (.) a_i)/da_i^T xbar */
+        for (int k = 0; k < W; ++k) ld_put(dtype, as_bar, i * W + k, ga[k], flags);
+    }
+    free(ls);
+    free(rs);
+    if (arg) *arg = -1;
+    if (zeros) *zeros = 0;
+    return O_OK;
+}
+
 int oracle_vjp_reduce(int op, int dtype, int64_t n, const void *as, const void *y_bar,
                       void *as_bar, void *y, int64_t *arg, int64_t *zeros, unsigned flags) {
     if ((dtype != O_F32 && dtype != O_F64) || n < 0) return O_EINVAL;
+    if (op == O_LINREC || op == O_MAT2)
+        return reduce_general(op, dtype, n, as, y_bar, as_bar, y, arg, zeros, flags);
     if (op != O_ADD && op != O_MUL && op != O_MIN && op != O_MAX) return O_EUNSUPPORTED;
     if (!y_bar || (n > 0 && (!as || !as_bar))) return O_EINVAL;
     LD ybar = ld_get(dtype, y_bar, 0);

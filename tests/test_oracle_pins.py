@@ -356,3 +356,58 @@ def test_f32_rounds_once():
     exact = [Fr(float(x[1])) * 3, Fr(1) * 3, Fr(float(x[1]))]
     assert got.dtype == np.float32
     assert [float(g) for g in got] == [float(np.float32(float(e))) for e in exact]
+
+
+# ------------------------------------------------ general reduce rule (f4)
+
+@pytest.mark.parametrize("op", ["linrec", "mat2"])
+def test_reduce_general_rule_is_scan_last(op):
+    """P:986-1013's general reduce rule for LINREC / MAT2 equals the scan's vjp
+    seeded only at the last element (scan-last == reduce) — two
+    independent code paths of the oracle (exclusive scans + map vs the
+    sequential return sweep of P:1153-1158)."""
+    import synth
+    import torch
+    gen = {"linrec": synth.linrec_inputs, "mat2": synth.mat2_inputs}[op]
+    a, _ = gen(1000)
+    a = a.numpy()
+    w = 2 if op == "linrec" else 4
+    ybar = np.arange(1, w + 1, dtype=np.float64) * 0.75
+    ab, y, _, _ = oracle.vjp_reduce(op, a, ybar)
+    seed = np.zeros_like(a)
+    seed[-w:] = ybar
+    ref, ys = oracle.vjp_scan(op, seed, a, want_ys=True)
+    assert np.allclose(ab, ref, rtol=1e-14, atol=0)
+    assert np.allclose(y, ys[-w:], rtol=1e-14, atol=0)
+
+
+@pytest.mark.parametrize("op", ["linrec", "mat2"])
+def test_reduce_general_rule_exact_central_fd(op):
+    """the general rule's adjoint equals the exact rational central difference of the
+    primal reduce on small integer inputs (every input direction)."""
+    rng = random.Random(5)
+    w = 2 if op == "linrec" else 4
+    n = 5
+    a = [Fr(rng.randint(-3, 3)) for _ in range(n * w)]
+    ybar = [Fr(rng.randint(-2, 2)) for _ in range(w)]
+
+    def prim(vals):
+        acc = [Fr(0), Fr(1)] if op == "linrec" else [Fr(1), Fr(0), Fr(0), Fr(1)]
+        for i in range(n):
+            e = vals[i * w:(i + 1) * w]
+            if op == "linrec":
+                acc = [e[0] + e[1] * acc[0], e[1] * acc[1]]
+            else:
+                acc = [acc[0] * e[0] + acc[1] * e[2], acc[0] * e[1] + acc[1] * e[3],
+                       acc[2] * e[0] + acc[3] * e[2], acc[2] * e[1] + acc[3] * e[3]]
+        return acc
+
+    exp = []
+    for k in range(n * w):  # the objective <ybar, reduce> is multilinear: exact central difference, h = 1
+        up = list(a); up[k] += 1
+        dn = list(a); dn[k] -= 1
+        fu = sum(y * v for y, v in zip(ybar, prim(up)))
+        fd = sum(y * v for y, v in zip(ybar, prim(dn)))
+        exp.append((fu - fd) / 2)
+    ab, _, _, _ = oracle.vjp_reduce(op, np.array([float(x) for x in a]), np.array([float(x) for x in ybar]))
+    assert ab.tolist() == [float(x) for x in exp]
