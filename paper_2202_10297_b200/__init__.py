@@ -228,19 +228,27 @@ def scan(op, ys_bar: torch.Tensor, as_: torch.Tensor | None = None, *, out: torc
 def reduce(op, as_: torch.Tensor, y_bar, *, out: torch.Tensor | None = None, want_y: bool = False,
            accumulate: bool = False):
     """as_bar of ``y = reduce op as_`` (sec 5.1).  y_bar: python float or a
-    1-element tensor.  Returns as_bar, or (as_bar, y, arg) if want_y (arg =
-    argmin/argmax for MIN/MAX, first zero index or -1 for MUL)."""
+    tensor of one element (W scalars for LINREC / MAT2, whose vjp is the
+    paper's general rule).  Returns as_bar, or (as_bar, y, arg) if
+    want_y (arg = argmin/argmax for MIN/MAX, first zero index or -1 for MUL,
+    -1 for ADD / LINREC / MAT2)."""
     o = _op(op)
+    w = WIDTH[o]
     host = not as_.is_cuda
     dev = _dev_of(as_, out)
     a = _to(as_, dev)
-    n = a.numel()
+    if a.numel() % w:
+        raise ValueError(f"as_ has {a.numel()} scalars, not a multiple of width {w}")
+    n = a.numel() // w
     if isinstance(y_bar, torch.Tensor):
-        yb = _to(y_bar.reshape(1).to(a.dtype), dev)
+        yb = _to(y_bar.reshape(-1).to(a.dtype), dev)
     else:
-        yb = torch.full((1,), float(y_bar), dtype=a.dtype, device=dev)
+        yb = torch.tensor([float(v) for v in (y_bar if hasattr(y_bar, "__len__") else [y_bar])],
+                          dtype=a.dtype).to(dev)
+    if yb.numel() != w:
+        raise ValueError(f"y_bar must hold {w} scalars")
     ab = _out_buf(out, a, dev, accumulate)
-    y = torch.empty(1, dtype=a.dtype, device=dev) if want_y else None
+    y = torch.empty(w, dtype=a.dtype, device=dev) if want_y else None
     arg = torch.empty(1, dtype=torch.int64, device=dev) if want_y else None
     L = lib()
     ws = workspace(L.vjp_reduce_workspace_bytes(o, _dt(a), n), dev)

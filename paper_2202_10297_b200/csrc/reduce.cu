@@ -14,6 +14,12 @@
 
 #include "common.cuh"
 
+namespace vjph {  // scan_abi.cu: the general reduce rule through the chunked scan kernels
+size_t reduce_general_ws(vjp_op op, vjp_dtype dtype, int64_t n);
+vjp_status reduce_general(vjp_op op, vjp_dtype dtype, int64_t n, const void *as, const void *y_bar, void *as_bar,
+                          void *y, void *ws, size_t ws_bytes, cudaStream_t stream, unsigned flags);
+}  // namespace vjph
+
 namespace vjpk {
 
 struct RRec {     // 32 bytes, also the multi-GPU exchange record
@@ -413,6 +419,7 @@ vjp_status run_bwd(vjp_op op, vjp_dtype dtype, const void *as, void *ab, const R
 extern "C" {
 
 size_t vjp_reduce_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_t n) {
+    if (op == VJP_LINREC || op == VJP_MAT2) return vjph::reduce_general_ws(op, dtype, n);
     if (!op_ok(op) || !dt_ok(dtype) || n < 0) return 0;
     return rlayout().total;
 }
@@ -421,6 +428,12 @@ size_t vjp_reduce_partial_bytes(void) { return sizeof(RRec); }
 
 vjp_status vjp_reduce(vjp_op op, vjp_dtype dtype, int64_t n, const void *as, const void *y_bar, void *as_bar,
                       void *y, int64_t *arg, void *ws, size_t ws_bytes, vjp_stream_t stream, unsigned flags) {
+    if (op == VJP_LINREC || op == VJP_MAT2) {  // the paper's general rule
+        if (arg && n > 0 && cudaMemsetAsync(arg, 0xff, 8, reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess)
+            return VJP_ECUDA;  // -1: no index for the general rule
+        return vjph::reduce_general(op, dtype, n, as, y_bar, as_bar, y, ws, ws_bytes,
+                                    reinterpret_cast<cudaStream_t>(stream), flags);
+    }
     vjp_status st = check(op, dtype, n, as, ws, ws_bytes);
     if (st != VJP_OK) return st;
     if (n == 0) return VJP_OK;

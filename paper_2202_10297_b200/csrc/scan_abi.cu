@@ -70,6 +70,47 @@ vjp_status check(const ScanCall &c, bool need_out) {
 }
 }  // namespace
 
+namespace vjph {
+size_t reduce_general_ws(vjp_op op, vjp_dtype dtype, int64_t n) {
+    Disp d = disp_for(op);
+    if (!d || (op != VJP_LINREC && op != VJP_MAT2) || !dtype_ok(dtype) || n < 0) return 0;
+    ScanCall c{};
+    c.op = op;
+    c.dtype = dtype;
+    c.n = n;
+    size_t out = 0;
+    d(kScanWs, c, &out);
+    return out;
+}
+vjp_status reduce_general(vjp_op op, vjp_dtype dtype, int64_t n, const void *as, const void *y_bar, void *as_bar,
+                          void *y, void *ws, size_t ws_bytes, cudaStream_t stream, unsigned flags) {
+    if ((op != VJP_LINREC && op != VJP_MAT2) || !dtype_ok(dtype) || n < 0) return VJP_EINVAL;
+    if (n == 0) return VJP_OK;
+    if (!as || !y_bar || !as_bar) return VJP_EINVAL;
+    const void *ptrs[3] = {as, as_bar, y};
+    for (const void *p : ptrs)
+        if (p && !aligned16(p)) return VJP_EALIGN;
+    if (as_bar == as) return VJP_EINVAL;
+    if (ws_bytes < reduce_general_ws(op, dtype, n) || !ws) return VJP_EWORKSPACE;
+    if (!aligned16(ws)) return VJP_EALIGN;
+    if (n / 1024 > (int64_t)1 << 30) return VJP_EINVAL;
+    ScanCall c{};
+    c.op = op;
+    c.dtype = dtype;
+    c.n = n;
+    c.as = as;
+    c.ys_bar = y_bar;  // the W scalars of the reduce's output adjoint
+    c.as_bar = as_bar;
+    c.ys = y;          // the primal reduction (nullable)
+    c.ws = ws;
+    c.ws_bytes = ws_bytes;
+    c.stream = stream;
+    c.flags = flags;
+    c.world = 1;
+    return disp_for(op)(kReduceGeneral, c, nullptr);
+}
+}  // namespace vjph
+
 extern "C" {
 
 size_t vjp_scan_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_t n) {

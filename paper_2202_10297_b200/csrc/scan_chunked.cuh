@@ -53,6 +53,7 @@ struct ChunkParams {
     const double *gathered;
     int32_t rank, world;
     int32_t global_first;
+    const void *ylast;  // YL kernels (general reduce rule): ys_bar = ylast at element n-1, 0 elsewhere
 };
 
 // per-CTA shared scratch beside the TMA stages (sized on the host with sizeof).
@@ -180,25 +181,42 @@ __device__ __forceinline__ typename Op::Val row_fwd(const unsigned char *sA, int
     return F;
 }
 
-// M_e0 o ... o M_{e0+EPR-1}; rs-independent operators only (chunked path)
-template <class Op, class T, bool FWD>
+// M_e0 o ... o M_{e0+EPR-1}; rs-independent operators only (chunked path).
+// YL: ys_bar is virtual — *yl at element n-1, zero elsewhere (general reduce).
+template <class Op, class T, bool FWD, bool YL = false>
 __device__ __forceinline__ typename Op::Map row_map(const unsigned char *sA, const unsigned char *sY, int t,
-                                                    int64_t e0, bool mask, int64_t n) {
+                                                    int64_t e0, bool mask, int64_t n,
+                                                    const typename Op::Val *yl = nullptr) {
     using G = Geo<Op, T>;
     typename Op::Map Tm = Op::map_id();
 #pragma unroll
     for (int g = G::NG - 1; g >= 0; --g) {
         uint32_t wa[G::GB / 4], wy[G::GB / 4];
         if (FWD) lds_group<G::GB>(sA, t, g, wa);
-        lds_group<G::GB>(sY, t, g, wy);
+        if (!YL) lds_group<G::GB>(sY, t, g, wy);
 #pragma unroll
         for (int e = G::EG - 1; e >= 0; --e) {
             typename Op::Val a = FWD ? dec<T, Op::W>(wa + e * (G::ES / 4)) : Op::fwd_id();
-            typename Op::Val y = dec<T, Op::W>(wy + e * (G::ES / 4));
+            typename Op::Val y;
+            if (YL) {
+#pragma unroll
+                for (int q = 0; q < Op::W; ++q) y.x[q] = (e0 + g * G::EG + e == n - 1) ? yl->x[q] : 0.0;
+            } else {
+                y = dec<T, Op::W>(wy + e * (G::ES / 4));
+            }
             if (!mask || e0 + g * G::EG + e < n) Tm = Op::extend(Tm, Op::fwd_id(), a, y);
         }
     }
     return Tm;
+}
+
+// the virtual ys_bar element of YL kernels (every thread keeps a copy)
+template <class Op, class T>
+__device__ __forceinline__ typename Op::Val load_ylast(const void *p) {
+    typename Op::Val v;
+#pragma unroll
+    for (int q = 0; q < Op::W; ++q) v.x[q] = p ? (double)static_cast<const T *>(p)[q] : 0.0;
+    return v;
 }
 
 // ---- warp-level scans over the NT row aggregates in shared memory ----------
@@ -298,7 +316,7 @@ __device__ __forceinline__ typename Op::Val warp_excl_rev_rows(double *m, typena
 // =============================================================================
 // K_R: per-tile / per-chunk aggregates
 // =============================================================================
-template <class Op, class T, int NT, int S, bool FWD, bool REV>
+template <class Op, class T, int NT, int S, bool FWD, bool REV, bool YL = false>
 __global__ void __launch_bounds__(NT, 1) scan_reduce(const __grid_constant__ CUtensorMap tm_as,
                                                      const __grid_constant__ CUtensorMap tm_yb,
                                                      const ChunkParams p) {
@@ -306,13 +324,14 @@ __global__ void __launch_bounds__(NT, 1) scan_reduce(const __grid_constant__ CUt
     using V = typename Op::Val;
     using M = typename Op::Map;
     constexpr int W = Op::W, NW = NT / 32, R = Op::W + Op::kMapD;
-    constexpr int NB = (FWD ? 1 : 0) + (REV ? 1 : 0);
+    constexpr int NB = (FWD ? 1 : 0) + ((REV && !YL) ? 1 : 0);
     constexpr int BUF = NT * kRowBytes, STG = NB * BUF;
     static_assert(NW >= 2, "needs a forward and a reverse scan warp");
 
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     ReduceSmem<Op, NT, S> &sm = *reinterpret_cast<ReduceSmem<Op, NT, S> *>(base + S * STG);
+    const V yl = YL ? load_ylast<Op, T>(p.ylast) : Op::fwd_id();
 
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     const int64_t c = blockIdx.x;
@@ -337,13 +356,13 @@ __global__ void __launch_bounds__(NT, 1) scan_reduce(const __grid_constant__ CUt
         if (last && p.tail_bytes) {
             if (t == (int)(p.full_rows - tile * NT)) {
                 if (FWD) load_partial_row(sA, t, p.as, p.full_rows, p.tail_bytes);
-                if (REV) load_partial_row(sY, t, p.ys_bar, p.full_rows, p.tail_bytes);
+                if (REV && !YL) load_partial_row(sY, t, p.ys_bar, p.full_rows, p.tail_bytes);
             }
             __syncthreads();
         }
         const int64_t e0 = (tile * NT + t) * G::EPR;
         V rowF = row_fwd<Op, T, FWD>(sA, t, e0, last, p.n);
-        M rowM = REV ? row_map<Op, T, FWD>(sA, sY, t, e0, last, p.n) : Op::map_id();
+        M rowM = REV ? row_map<Op, T, FWD, YL>(sA, sY, t, e0, last, p.n, &yl) : Op::map_id();
         __syncthreads();  // every row read its data (stage s is free) and the scan warps are done with the scratch
         if (t == 0 && i + S < k) issue_tile<NT, NB>(p, tile + S, &sm.bar[s], sA, m0, &tm_yb, &tm_yb);
         if (FWD) put_v<Op, NT>(sm.rv, t, rowF);
@@ -396,7 +415,7 @@ __global__ void __launch_bounds__(NT, 1) scan_reduce(const __grid_constant__ CUt
 // =============================================================================
 // K_C: return sweep over the chunk, right to left
 // =============================================================================
-template <class Op, class T, int NT, int S, bool FWD, bool ACC, bool YS>
+template <class Op, class T, int NT, int S, bool FWD, bool ACC, bool YS, bool YL = false>
 __global__ void __launch_bounds__(NT, 1) scan_apply(const __grid_constant__ CUtensorMap tm_as,
                                                     const __grid_constant__ CUtensorMap tm_yb,
                                                     const __grid_constant__ CUtensorMap tm_ab,
@@ -406,20 +425,23 @@ __global__ void __launch_bounds__(NT, 1) scan_apply(const __grid_constant__ CUte
     using V = typename Op::Val;
     using M = typename Op::Map;
     constexpr int W = Op::W, NW = NT / 32;
-    constexpr int NB = (FWD ? 1 : 0) + 1 + (ACC ? 1 : 0);
-    constexpr int BUF = NT * kRowBytes, STG = NB * BUF;
+    // loaded buffers: [A][Y][C] (output written over Y); YL: [A][C] plus an
+    // output-only buffer O after them
+    constexpr int NB = YL ? (FWD ? 1 : 0) + (ACC ? 1 : 0) : (FWD ? 1 : 0) + 1 + (ACC ? 1 : 0);
+    constexpr int NBA = YL ? NB + 1 : NB;
+    constexpr int BUF = NT * kRowBytes, STG = NBA * BUF;
     static_assert(NW >= 2, "needs a forward and a reverse scan warp");
 
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     ApplySmem<Op, NT, S> &sm = *reinterpret_cast<ApplySmem<Op, NT, S> *>(base + S * STG);
+    const V yl = YL ? load_ylast<Op, T>(p.ylast) : Op::fwd_id();
 
     const int t = threadIdx.x, warp = t >> 5;
     const int64_t c = blockIdx.x;
     const int64_t t0 = chunk_begin(p, c), t1 = chunk_begin(p, c + 1), k = t1 - t0;
-    // stage buffer order: [A][Y][C]
-    const CUtensorMap *m0 = FWD ? &tm_as : &tm_yb;
-    const CUtensorMap *m1 = FWD ? &tm_yb : &tm_ab;
+    const CUtensorMap *m0 = YL ? (FWD ? &tm_as : &tm_ab) : (FWD ? &tm_as : &tm_yb);
+    const CUtensorMap *m1 = YL ? &tm_ab : (FWD ? &tm_yb : &tm_ab);
     const CUtensorMap *m2 = &tm_ab;
     if (t == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&sm.bar[s], 1);
@@ -477,15 +499,16 @@ __global__ void __launch_bounds__(NT, 1) scan_apply(const __grid_constant__ CUte
         }
         mbar_wait(&sm.bar[s], (uint32_t)((i / S) & 1));
         unsigned char *sA = base + s * STG;
-        unsigned char *sY = sA + (FWD ? BUF : 0);
-        unsigned char *sC = sY + BUF;
+        unsigned char *sY = sA + (FWD ? BUF : 0);                                  // not YL
+        unsigned char *sC = YL ? sA + (FWD ? BUF : 0) : sY + BUF;
+        unsigned char *sO = YL ? sA + (size_t)NB * BUF : sY;                       // output tile
         const bool last = (tile == p.ntiles - 1);
         const int prow = (int)(p.full_rows - tile * NT);
         const bool has_partial = last && p.tail_bytes && t == prow;
         if (last && p.tail_bytes) {
             if (has_partial) {
                 if (FWD) load_partial_row(sA, t, p.as, p.full_rows, p.tail_bytes);
-                load_partial_row(sY, t, p.ys_bar, p.full_rows, p.tail_bytes);
+                if (!YL) load_partial_row(sY, t, p.ys_bar, p.full_rows, p.tail_bytes);
                 if (ACC) load_partial_row(sC, t, p.as_bar, p.full_rows, p.tail_bytes);
             }
             __syncthreads();
@@ -494,7 +517,7 @@ __global__ void __launch_bounds__(NT, 1) scan_apply(const __grid_constant__ CUte
 
         // phase 1: row aggregates -> shared memory
         if (FWD) put_v<Op, NT>(sm.rv, t, row_fwd<Op, T, FWD>(sA, t, e0, last, p.n));
-        put_m<Op, NT>(sm.rm, t, row_map<Op, T, FWD>(sA, sY, t, e0, last, p.n));
+        put_m<Op, NT>(sm.rm, t, row_map<Op, T, FWD, YL>(sA, sY, t, e0, last, p.n, &yl));
         __syncthreads();
         // block scans: warp 0 forward (rs entering each row), warp 1 reverse (H entering each row)
         if (FWD && warp == 0) warp_excl_fwd_rows<Op, NT>(sm.rv, Ftile);
@@ -525,13 +548,19 @@ __global__ void __launch_bounds__(NT, 1) scan_apply(const __grid_constant__ CUte
         for (int g = G::NG - 1; g >= 0; --g) {
             uint32_t wa[G::GB / 4], wy[G::GB / 4], wc[G::GB / 4], wo[G::GB / 4], wz[G::GB / 4];
             if (FWD) lds_group<G::GB>(sA, t, g, wa);
-            lds_group<G::GB>(sY, t, g, wy);
+            if (!YL) lds_group<G::GB>(sY, t, g, wy);
             if (ACC) lds_group<G::GB>(sC, t, g, wc);
 #pragma unroll
             for (int e = G::EG - 1; e >= 0; --e) {
                 const int q = g * G::EG + e;
                 V a = FWD ? dec<T, W>(wa + e * (G::ES / 4)) : Op::fwd_id();
-                V y = dec<T, W>(wy + e * (G::ES / 4));
+                V y;
+                if (YL) {
+#pragma unroll
+                    for (int z = 0; z < W; ++z) y.x[z] = (e0 + q == p.n - 1) ? yl.x[z] : 0.0;
+                } else {
+                    y = dec<T, W>(wy + e * (G::ES / 4));
+                }
                 V gv;
 #pragma unroll
                 for (int z = 0; z < W; ++z) gv.x[z] = y.x[z] + Xr.x[z];  // rbar_i = ybar_i + H_{i+1}
@@ -546,18 +575,18 @@ __global__ void __launch_bounds__(NT, 1) scan_apply(const __grid_constant__ CUte
                 if (YS) enc<T, W>(Op::fwd(rsp[q], a), wz + e * (G::ES / 4));
                 if (!last || e0 + q < p.n) Xr = Op::pass_left(rsp[q], a, gv);  // H_i = J_L^T rbar_i
             }
-            sts_group<G::GB>(sY, t, g, wo);
+            sts_group<G::GB>(sO, t, g, wo);
             if (YS) sts_group<G::GB>(sA, t, g, wz);
         }
         if (has_partial) {
-            store_partial_row(sY, t, p.as_bar, p.full_rows, p.tail_bytes);
+            store_partial_row(sO, t, p.as_bar, p.full_rows, p.tail_bytes);
             if (YS) store_partial_row(sA, t, p.ys, p.full_rows, p.tail_bytes);
         }
         fence_proxy_async_smem();
         __syncthreads();
         if (t == 0) {
             if (chunk_tile_rows<NT>(p, tile) > 0) {
-                tma_store_2d(&tm_ab, sY, 0, (int)(tile * NT));
+                tma_store_2d(&tm_ab, sO, 0, (int)(tile * NT));
                 if (YS) tma_store_2d(&tm_ys, sA, 0, (int)(tile * NT));
             }
             tma_store_commit();
@@ -570,6 +599,21 @@ __global__ void __launch_bounds__(NT, 1) scan_apply(const __grid_constant__ CUte
         }
     }
     if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// ordered combination of the chunk records' forward parts (the primal
+// reduction of the general reduce rule), one CTA
+template <class Op, class T, int NT>
+__global__ void __launch_bounds__(NT) scan_chunks_total(const ChunkParams p, T *y) {
+    __shared__ typename Op::Val vs[NT / 32 + 1];
+    __shared__ typename Op::Map ms[NT / 32 + 1];
+    typename Op::Val F;
+    typename Op::Map M;
+    range_reduce<Op, NT>(p.chunkRec, 0, p.nchunks, vs, ms, F, M);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < Op::W; ++q) y[q] = (T)F.x[q];
+    }
 }
 
 }  // namespace vjpk

@@ -30,7 +30,7 @@ struct ScanCall {
     const void *gathered;  // finish phase: world records (device)
 };
 
-enum ScanPhase { kScanWs = 0, kScanPartial = 1, kScanFinish = 2, kScanPartialBytes = 3 };
+enum ScanPhase { kScanWs = 0, kScanPartial = 1, kScanFinish = 2, kScanPartialBytes = 3, kReduceGeneral = 4 };
 
 template <class Op, class T>
 struct ScanImpl {
@@ -389,6 +389,48 @@ struct ScanImpl {
         return ys ? launch_sweep<true, false, true>(c, L) : launch_sweep<true, false, false>(c, L);
     }
 
+    // ---------------- general reduce rule, LINREC / MAT2 ----------------
+    // vjp of y = reduce (.) e as equals the scan's return sweep seeded only at
+    // the last element (scan-last == reduce): the chunked kernels run
+    // with a VIRTUAL ys_bar (c.ys_bar -> the W scalars of y_bar at element
+    // n-1, zero elsewhere; YL) — nothing of ys_bar is read from memory, so the
+    // sweep moves `as` twice and writes as_bar once (MAT2 96 B/elem, against
+    // the >= 5 accesses per element of the paper's two-scans-and-a-map).
+    static vjp_status reduce_general(const ScanCall &c) {
+        if constexpr (Op::kRevNeedsRs || std::is_same<Op, vjpk::OpAdd>::value) {
+            return VJP_EUNSUPPORTED;
+        } else {
+            Layout L = layout(c.n);
+            const bool acc = (c.flags & VJP_ACCUMULATE) != 0;
+            const int G = nchunks_for(L, true, acc);
+            vjpk::ChunkParams p = cparams(c, L, G);
+            p.ylast = c.ys_bar;
+            p.ys_bar = nullptr;
+            p.ys = nullptr;
+            CUtensorMap ma, my, mab, mys;
+            const bool f64 = sizeof(T) == 8;
+            if (!make_row_tmap(&ma, c.as, p.full_rows, f64, NTC) || !make_row_tmap(&my, nullptr, 0, f64, NTC) ||
+                !make_row_tmap(&mab, c.as_bar, p.full_rows, f64, NTC) || !make_row_tmap(&mys, nullptr, 0, f64, NTC))
+                return VJP_ECUDA;
+            auto kr = vjpk::scan_reduce<Op, T, NTC, SC, true, true, true>;
+            const size_t smr = smem_r(1);
+            set_smem(kr, smr);
+            kr<<<(unsigned)p.nchunks, NTC, smr, c.stream>>>(ma, my, p);
+            auto kc = acc ? vjpk::scan_apply<Op, T, NTC, SC, true, true, false, true>
+                          : vjpk::scan_apply<Op, T, NTC, SC, true, false, false, true>;
+            const size_t sma = smem_a(acc ? 3 : 2);
+            set_smem(kc, sma);
+            kc<<<(unsigned)p.nchunks, NTC, sma, c.stream>>>(ma, my, mab, mys, p);
+            int launches = 2;
+            if (c.ys) {  // the primal reduction: ordered combination of the chunk records
+                vjpk::scan_chunks_total<Op, T, NTC><<<1, NTC, 0, c.stream>>>(p, static_cast<T *>(c.ys));
+                ++launches;
+            }
+            count_launch(launches);
+            return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+        }
+    }
+
     static vjp_status partial(const ScanCall &c) {
         if constexpr (!Op::kRevNeedsRs) {
             if (use_sweep(c)) return partial_sw(c);
@@ -454,10 +496,12 @@ vjp_status scan_dispatch(int phase, const ScanCall &c, size_t *out) {
     if (c.dtype == VJP_F64) {
         using I = ScanImpl<Op, double>;
         if (phase == kScanWs) { *out = I::layout(c.n).total; return VJP_OK; }
+        if (phase == kReduceGeneral) return I::reduce_general(c);
         return phase == kScanPartial ? I::partial(c) : I::finish(c);
     }
     using I = ScanImpl<Op, float>;
     if (phase == kScanWs) { *out = I::layout(c.n).total; return VJP_OK; }
+    if (phase == kReduceGeneral) return I::reduce_general(c);
     return phase == kScanPartial ? I::partial(c) : I::finish(c);
 }
 
@@ -467,5 +511,10 @@ vjp_status scan_dispatch_min(int, const ScanCall &, size_t *);
 vjp_status scan_dispatch_max(int, const ScanCall &, size_t *);
 vjp_status scan_dispatch_linrec(int, const ScanCall &, size_t *);
 vjp_status scan_dispatch_mat2(int, const ScanCall &, size_t *);
+
+// general reduce rule for LINREC / MAT2 (reduce.cu routes vjp_reduce here)
+size_t reduce_general_ws(vjp_op op, vjp_dtype dtype, int64_t n);
+vjp_status reduce_general(vjp_op op, vjp_dtype dtype, int64_t n, const void *as, const void *y_bar, void *as_bar,
+                          void *y, void *ws, size_t ws_bytes, cudaStream_t stream, unsigned flags);
 
 }  // namespace vjph

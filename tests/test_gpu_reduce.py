@@ -112,3 +112,39 @@ def test_config3_full_size(case):
         if ref_z:
             assert int(arg.item()) == ref_arg
         assert_close(got, ref_ab, np.float32, what=case)
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32], ids=["f64", "f32"])
+@pytest.mark.parametrize("op", ["linrec", "mat2"])
+def test_reduce_general_rule(op, dt):
+    """LINREC / MAT2 reduce (the paper's general rule) through the
+    chunked kernels with a virtual ys_bar, against the oracle's literal
+    exclusive-scans-and-map; sizes from one element through ragged tiles;
+    the primal y and ACCUMULATE."""
+    import synth
+    gen = {"linrec": synth.linrec_inputs, "mat2": synth.mat2_inputs}[op]
+    w = 2 if op == "linrec" else 4
+    td = torch.float64 if dt == np.float64 else torch.float32
+    ybar = torch.tensor([0.75, -1.25, 0.5, 2.0][:w], dtype=td)
+    def inputs(n):
+        a, _ = gen(n, dtype=torch.float64)
+        if op == "linrec":  # prod(c) of 10^6 draws from U(0.5, 1) underflows: keep c near 1
+            a = a.reshape(n, 2).clone()
+            a[:, 1] = 1.0 + (synth.uniform(n, 13, dtype=torch.float64) - 0.5) / 256
+            a = a.reshape(-1)
+        return a.to(td)
+
+    for n in (1, 2, 33, 1023, 1024, 4097, 100_003, 1_000_001):
+        a = inputs(n)
+        ref, ry, _, _ = oracle.vjp_reduce(op, a.numpy(), ybar.numpy())
+        got, y, arg = vjp.reduce(op, a.to("cuda"), ybar.to("cuda"), want_y=True)
+        assert_close(got.cpu().numpy(), ref, dt, what=f"general reduce {op} n={n}")
+        assert_close(y.cpu().numpy(), np.asarray(ry), dt, what=f"general reduce y {op} n={n}")
+        assert int(arg.item()) == -1
+    n = 70_001
+    a = inputs(n)
+    base = synth.uniform(n * w, 12, dtype=td)
+    ref, _, _, _ = oracle.vjp_reduce(op, a.numpy(), ybar.numpy(), out=base.numpy().copy(), accumulate=True)
+    out = base.to("cuda")
+    vjp.reduce(op, a.to("cuda"), ybar.to("cuda"), out=out, accumulate=True)
+    assert_close(out.cpu().numpy(), ref, dt, what=f"general reduce accumulate {op}")
