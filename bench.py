@@ -383,6 +383,22 @@ def run_extra(args):
                 o = torch.empty(N28, dtype=torch.float64, device=dev)
                 cases.append((f"rbi {op.upper()} f64 n=2^28 m={m}", N28, nb * N28,
                               (lambda op=op, inds=inds, a=a, hb=hb, o=o: vjp.reduce_by_index(op, inds, a, hb, out=o))))
+    if w in ("batched", "all"):
+        # vectorised scans: ADD 2^20 x 64, LINREC 2^20 x 32 (f64)
+        ya = synth.scan_add_seed((1 << 20) * 64, device=dev)
+        oa = torch.empty_like(ya)
+        cases.append(("batched scan ADD f64 n=2^20 w=64", (1 << 20) * 64, 16 * (1 << 20) * 64,
+                      lambda ya=ya, oa=oa: vjp.scan_batched("add", ya, width=64, out=oa)))
+        al, yl = synth.linrec_inputs((1 << 20) * 32, device=dev)
+        ol = torch.empty_like(yl)
+        cases.append(("batched scan LINREC f64 n=2^20 w=32", (1 << 20) * 32, 64 * (1 << 20) * 32,
+                      lambda al=al, yl=yl, ol=ol: vjp.scan_batched("linrec", yl, al, width=32, out=ol)))
+        # general reduce rule: MAT2 reduce, n = 2^26 f64 (as read twice + as_bar: 96 B/elem)
+        am, _ = synth.mat2_inputs(N26, device=dev)
+        om = torch.empty_like(am)
+        ybm = torch.tensor([1.0, 0.5, -0.5, 2.0], dtype=torch.float64, device=dev)
+        cases.append(("general reduce MAT2 f64 n=2^26", N26, 96 * N26,
+                      lambda am=am, om=om, ybm=ybm: vjp.reduce("mat2", am, ybm, out=om)))
     if w in ("kmeans", "all"):
         # config 5: n = 10^6 points, d = 64, k = 1024, f64 (one call: forward
         # distance/argmin on the FP64 tensor pipe + the return sweep)
@@ -421,7 +437,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", default="config2",
-                    choices=["config2", "scan_add", "scan_linrec30", "reduce", "rbi", "kmeans", "all"],
+                    choices=["config2", "scan_add", "scan_linrec30", "reduce", "rbi", "kmeans", "batched", "all"],
                     help="config2 = the headline line; the others print per-call extra lines")
     args = ap.parse_args()
     if args.warmup < 3:
