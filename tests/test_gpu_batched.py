@@ -63,3 +63,8 @@ def test_batched_minmax_unsupported():
     yb = torch.ones(100, dtype=torch.float64, device=DEV)
     with pytest.raises(vjp.VjpError):
         vjp.scan_batched("min", yb, yb.clone(), width=4)
+
+
+def test_batched_empty():
+    yb = torch.empty(0, dtype=torch.float64, device=DEV)
+    assert vjp.scan_batched("add", yb, width=3).numel() == 0

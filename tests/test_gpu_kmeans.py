@@ -139,3 +139,11 @@ def test_kmeans_config5_full_size_sampled():
     assert float(((got["cbar"] - ref_cbar).abs() / (scale + 1e-300)).max()) <= 1e-10
     cost = ((P - C[a]) ** 2).sum()
     assert abs(float(got["cost"]) - float(cost)) <= 1e-10 * float(cost)
+
+
+def test_kmeans_no_points():
+    """n = 0: zero gradient / Hessian / counts / cost (reading R7: empty input)."""
+    C = torch.randn(7, 5, dtype=torch.float64, device=DEV)
+    r = vjp.kmeans(torch.empty(0, 5, dtype=torch.float64, device=DEV), C, 1.0)
+    assert torch.equal(r["cbar"], torch.zeros_like(C)) and torch.equal(r["hdiag"], torch.zeros_like(C))
+    assert int(r["counts"].sum()) == 0 and float(r["cost"]) == 0.0

@@ -148,3 +148,13 @@ def test_reduce_general_rule(op, dt):
     out = base.to("cuda")
     vjp.reduce(op, a.to("cuda"), ybar.to("cuda"), out=out, accumulate=True)
     assert_close(out.cpu().numpy(), ref, dt, what=f"general reduce accumulate {op}")
+
+
+def test_reduce_general_rule_empty_and_single():
+    """n = 0 is a no-op (R7); n = 1: abar_0 = ybar (J_R(e, a) = I for lin_o and the 2x2 product)."""
+    yb = torch.tensor([0.5, -2.0, 1.0, 3.0], dtype=torch.float64, device="cuda")
+    assert vjp.reduce("mat2", torch.empty(0, dtype=torch.float64, device="cuda"), yb).numel() == 0
+    a = torch.tensor([0.3, 0.7, 0.2, 0.8], dtype=torch.float64, device="cuda")
+    assert torch.equal(vjp.reduce("mat2", a, yb), yb)
+    a2 = torch.tensor([0.25, 0.5], dtype=torch.float64, device="cuda")
+    assert torch.equal(vjp.reduce("linrec", a2, yb[:2]), yb[:2])
