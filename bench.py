@@ -376,6 +376,21 @@ def run_extra(args):
                       lambda a=a, o=o: vjp.reduce("min", a, 1.5, out=o)))
         cases.append(("reduce MIN f32 n=2^30 accumulate", N30, 4 * N30,
                       lambda a=a, o=o: vjp.reduce("min", a, 1.5, out=o, accumulate=True)))
+        cases.append(("reduce ADD f32 n=2^30 (broadcast of ybar, 4 B/elem)", N30, 4 * N30,
+                      lambda a=a, o=o: vjp.reduce("add", a, 1.5, out=o)))
+        del a
+        # scatter (a14): m = 2^24 distinct targets into n = 2^28 f64, in place (O(m):
+        # gather 8 B + zero 8 B + index 8 B + vs_bar 8 B per target)
+        is_, ybs = synth.scatter_inputs(N28, 1 << 24, device=dev)
+        vs = torch.empty(1 << 24, dtype=torch.float64, device=dev)
+        cases.append(("scatter in place f64 n=2^28 m=2^24 (32 B/target)", 1 << 24, 32 * (1 << 24),
+                      lambda is_=is_, ybs=ybs, vs=vs: vjp.scatter(is_, ybs, in_place=True, vs_out=vs)))
+        # MIN scan (pick-left subgradient, look-back kernels: the reverse maps need rs)
+        am = synth.min_inputs(N26, dtype=torch.float64, device=dev)
+        ym = synth.uniform(N26, 10, device=dev)
+        omn = torch.empty_like(ym)
+        cases.append(("scan MIN f64 n=2^26 (look-back, 24 B/elem)", N26, 24 * N26,
+                      lambda am=am, ym=ym, omn=omn: vjp.scan("min", ym, am, out=omn)))
     if w in ("rbi", "all"):
         for m in (1000, 1_000_000):
             for op, nb in (("add", 12), ("mul", 32), ("max", 20)):
