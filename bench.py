@@ -385,11 +385,11 @@ def run_extra(args):
         vs = torch.empty(1 << 24, dtype=torch.float64, device=dev)
         cases.append(("scatter in place f64 n=2^28 m=2^24 (32 B/target)", 1 << 24, 32 * (1 << 24),
                       lambda is_=is_, ybs=ybs, vs=vs: vjp.scatter(is_, ybs, in_place=True, vs_out=vs)))
-        # MIN scan (pick-left subgradient, look-back kernels: the reverse maps need rs)
+        # MIN scan (pick-left subgradient; the reverse maps need rs: K_F + K_R' + K_C)
         am = synth.min_inputs(N26, dtype=torch.float64, device=dev)
         ym = synth.uniform(N26, 10, device=dev)
         omn = torch.empty_like(ym)
-        cases.append(("scan MIN f64 n=2^26 (look-back, 24 B/elem)", N26, 24 * N26,
+        cases.append(("scan MIN f64 n=2^26 (chunked rs-dependent path, 24 B/elem method)", N26, 24 * N26,
                       lambda am=am, ym=ym, omn=omn: vjp.scan("min", ym, am, out=omn)))
     if w in ("rbi", "all"):
         for m in (1000, 1_000_000):

@@ -219,6 +219,41 @@ __device__ __forceinline__ typename Op::Val load_ylast(const void *p) {
     return v;
 }
 
+// rs-DEPENDENT operators (MIN/MAX: the Jacobians pick a side by comparing
+// rs_{i-1} with a_i): re-execute the primal over the row from `rs` (the prefix
+// entering the row), then compose the maps right to left with the true rs.
+template <class Op, class T>
+__device__ __forceinline__ typename Op::Map row_map_rs(const unsigned char *sA, const unsigned char *sY, int t,
+                                                       int64_t e0, bool mask, int64_t n, typename Op::Val rs) {
+    using G = Geo<Op, T>;
+    typename Op::Val rsp[G::EPR];
+#pragma unroll
+    for (int g = 0; g < G::NG; ++g) {
+        uint32_t wa[G::GB / 4];
+        lds_group<G::GB>(sA, t, g, wa);
+#pragma unroll
+        for (int e = 0; e < G::EG; ++e) {
+            const int q = g * G::EG + e;
+            rsp[q] = rs;
+            if (!mask || e0 + q < n) rs = Op::fwd(rs, dec<T, Op::W>(wa + e * (G::ES / 4)));
+        }
+    }
+    typename Op::Map Tm = Op::map_id();
+#pragma unroll
+    for (int g = G::NG - 1; g >= 0; --g) {
+        uint32_t wa[G::GB / 4], wy[G::GB / 4];
+        lds_group<G::GB>(sA, t, g, wa);
+        lds_group<G::GB>(sY, t, g, wy);
+#pragma unroll
+        for (int e = G::EG - 1; e >= 0; --e) {
+            const int q = g * G::EG + e;
+            if (!mask || e0 + q < n)
+                Tm = Op::extend(Tm, rsp[q], dec<T, Op::W>(wa + e * (G::ES / 4)), dec<T, Op::W>(wy + e * (G::ES / 4)));
+        }
+    }
+    return Tm;
+}
+
 // ---- warp-level scans over the NT row aggregates in shared memory ----------
 // (executed by one full warp; lane l owns rows [l*K, l*K + K), K = NT/32)
 
@@ -413,9 +448,83 @@ __global__ void __launch_bounds__(NT, 1) scan_reduce(const __grid_constant__ CUt
 }
 
 // =============================================================================
+// K_R' (rs-dependent operators): per chunk the composed reverse map with the
+// TRUE rs — the forward prefix entering every tile (tileP, from the forward
+// pre-pass K_F + scan_tile_prefix) and a warp-0 row scan give rs entering each
+// row; the maps are then built as for the other operators.
+// =============================================================================
+template <class Op, class T, int NT, int S>
+__global__ void __launch_bounds__(NT, 1) scan_reduce_rs(const __grid_constant__ CUtensorMap tm_as,
+                                                        const __grid_constant__ CUtensorMap tm_yb,
+                                                        const ChunkParams p) {
+    using G = Geo<Op, T>;
+    using V = typename Op::Val;
+    using M = typename Op::Map;
+    constexpr int W = Op::W, NW = NT / 32, R = Op::W + Op::kMapD;
+    constexpr int NB = 2;
+    constexpr int BUF = NT * kRowBytes, STG = NB * BUF;
+    static_assert(NW >= 2, "needs a forward and a reverse scan warp");
+
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    ReduceSmem<Op, NT, S> &sm = *reinterpret_cast<ReduceSmem<Op, NT, S> *>(base + S * STG);
+
+    const int t = threadIdx.x, warp = t >> 5;
+    const int64_t c = blockIdx.x;
+    const int64_t t0 = chunk_begin(p, c), t1 = chunk_begin(p, c + 1), k = t1 - t0;
+    if (t == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&sm.bar[s], 1);
+        fence_mbar_init();
+        for (int s = 0; s < S && s < k; ++s) issue_tile<NT, NB>(p, t0 + s, &sm.bar[s], base + s * STG, &tm_as, &tm_yb, &tm_yb);
+    }
+    __syncthreads();
+
+    M Mc = Op::map_id();  // kept by warp 1
+    for (int64_t i = 0; i < k; ++i) {
+        const int64_t tile = t0 + i;
+        const int s = (int)(i % S);
+        V Ftile = Op::fwd_id();
+        if (warp == 0) {
+#pragma unroll
+            for (int q = 0; q < W; ++q) Ftile.x[q] = ld_cg(p.tileP + tile * W + q);
+        }
+        mbar_wait(&sm.bar[s], (uint32_t)((i / S) & 1));
+        unsigned char *sA = base + s * STG;
+        unsigned char *sY = sA + BUF;
+        const bool last = (tile == p.ntiles - 1);
+        if (last && p.tail_bytes) {
+            if (t == (int)(p.full_rows - tile * NT)) {
+                load_partial_row(sA, t, p.as, p.full_rows, p.tail_bytes);
+                load_partial_row(sY, t, p.ys_bar, p.full_rows, p.tail_bytes);
+            }
+            __syncthreads();
+        }
+        const int64_t e0 = (tile * NT + t) * G::EPR;
+        put_v<Op, NT>(sm.rv, t, row_fwd<Op, T, true>(sA, t, e0, last, p.n));
+        __syncthreads();  // (also: warp 1 is done with the previous tile's maps)
+        if (warp == 0) warp_excl_fwd_rows<Op, NT>(sm.rv, Ftile);
+        __syncthreads();
+        M rowM = row_map_rs<Op, T>(sA, sY, t, e0, last, p.n, get_v<Op, NT>(sm.rv, t));
+        __syncthreads();  // stage s consumed
+        if (t == 0 && i + S < k) issue_tile<NT, NB>(p, tile + S, &sm.bar[s], sA, &tm_as, &tm_yb, &tm_yb);
+        put_m<Op, NT>(sm.rm, t, rowM);
+        __syncthreads();
+        if (warp == 1) Mc = Op::compose(Mc, warp_reduce_rev_rows<Op, NT>(sm.rm));
+    }
+    if (t == 32) {
+        double rec[R];
+        const V id = Op::fwd_id();
+#pragma unroll
+        for (int q = 0; q < W; ++q) rec[q] = id.x[q];
+        map_to<Op>(Mc, rec + W);
+        st_rec<R>(p.chunkRec + c * R, rec);
+    }
+}
+
+// =============================================================================
 // K_C: return sweep over the chunk, right to left
 // =============================================================================
-template <class Op, class T, int NT, int S, bool FWD, bool ACC, bool YS, bool YL = false>
+template <class Op, class T, int NT, int S, bool FWD, bool ACC, bool YS, bool YL = false, bool RS = false>
 __global__ void __launch_bounds__(NT, 1) scan_apply(const __grid_constant__ CUtensorMap tm_as,
                                                     const __grid_constant__ CUtensorMap tm_yb,
                                                     const __grid_constant__ CUtensorMap tm_ab,
@@ -462,7 +571,7 @@ __global__ void __launch_bounds__(NT, 1) scan_apply(const __grid_constant__ CUte
         range_reduce<Op, NT>(p.chunkRec, 0, c, sm.vs, sm.ms, Fpre, Mdummy);
         range_reduce<Op, NT>(p.chunkRec, c + 1, p.nchunks, sm.vs, sm.ms, Fdummy, Mpost);
         X = Op::apply(Mpost, Hin);
-        if constexpr (FWD) {
+        if constexpr (FWD && !RS) {  // (RS: tileP comes from the forward pre-pass)
             // forward exclusive prefix of every tile of the chunk -> tileP
             V Fch = Op::fwd(Fsh, Fpre);
             const int64_t per = (k + NT - 1) / NT;
@@ -515,14 +624,26 @@ __global__ void __launch_bounds__(NT, 1) scan_apply(const __grid_constant__ CUte
         }
         const int64_t e0 = (tile * NT + t) * G::EPR;
 
-        // phase 1: row aggregates -> shared memory
-        if (FWD) put_v<Op, NT>(sm.rv, t, row_fwd<Op, T, FWD>(sA, t, e0, last, p.n));
-        put_m<Op, NT>(sm.rm, t, row_map<Op, T, FWD, YL>(sA, sY, t, e0, last, p.n, &yl));
-        __syncthreads();
-        // block scans: warp 0 forward (rs entering each row), warp 1 reverse (H entering each row)
-        if (FWD && warp == 0) warp_excl_fwd_rows<Op, NT>(sm.rv, Ftile);
-        if (warp == 1) X = warp_excl_rev_rows<Op, NT>(sm.rm, X);
-        __syncthreads();
+        if constexpr (RS) {
+            // rs-dependent maps: forward row scan first, then maps with the true rs
+            put_v<Op, NT>(sm.rv, t, row_fwd<Op, T, true>(sA, t, e0, last, p.n));
+            __syncthreads();
+            if (warp == 0) warp_excl_fwd_rows<Op, NT>(sm.rv, Ftile);
+            __syncthreads();
+            put_m<Op, NT>(sm.rm, t, row_map_rs<Op, T>(sA, sY, t, e0, last, p.n, get_v<Op, NT>(sm.rv, t)));
+            __syncthreads();
+            if (warp == 1) X = warp_excl_rev_rows<Op, NT>(sm.rm, X);
+            __syncthreads();
+        } else {
+            // phase 1: row aggregates -> shared memory
+            if (FWD) put_v<Op, NT>(sm.rv, t, row_fwd<Op, T, FWD>(sA, t, e0, last, p.n));
+            put_m<Op, NT>(sm.rm, t, row_map<Op, T, FWD, YL>(sA, sY, t, e0, last, p.n, &yl));
+            __syncthreads();
+            // block scans: warp 0 forward (rs entering each row), warp 1 reverse (H entering each row)
+            if (FWD && warp == 0) warp_excl_fwd_rows<Op, NT>(sm.rv, Ftile);
+            if (warp == 1) X = warp_excl_rev_rows<Op, NT>(sm.rm, X);
+            __syncthreads();
+        }
 
         // phase 2: re-execute the primal scan over the row, then outputs right to left
         V rsp[G::EPR];

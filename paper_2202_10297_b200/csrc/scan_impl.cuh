@@ -431,7 +431,66 @@ struct ScanImpl {
         }
     }
 
+    // ---------------- chunked path for rs-dependent operators (MIN / MAX) ----------------
+    // K_F (forward aggregates, reads as) -> scan_tile_prefix (tileP) -> K_R'
+    // (reverse-map chunk records with the true rs, reads as + ys_bar) -> K_C (RS
+    // variant).  Three streaming passes (f64: 8 + 16 + 24 B/elem) instead of the
+    // latency-bound single-sweep look-back.  Single GPU.
+    static bool use_rs_chunked(const ScanCall &c) {
+        return Op::kRevNeedsRs && c.world == 1 && !(c.flags & VJP_SCAN_LOOKBACK);
+    }
+    static vjp_status partial_rs(const ScanCall &c) {
+        Layout L = layout(c.n);
+        vjpk::ChunkParams p = cparams(c, L, nchunks_fwd(L));
+        CUtensorMap ma, my, mab, mys;
+        if (!maps_c(c, p.full_rows, &ma, &my, &mab, &mys)) return VJP_ECUDA;
+        auto k = vjpk::scan_reduce<Op, T, NTC, SC, true, false>;
+        size_t sm = smem_r(1);
+        set_smem(k, sm);
+        k<<<(unsigned)p.nchunks, NTC, sm, c.stream>>>(ma, my, p);
+        count_launch();
+        return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+    }
+    template <bool ACC, bool YS>
+    static vjp_status launch_apply_rs(const ScanCall &c, const vjpk::ChunkParams &p, const CUtensorMap &ma,
+                                      const CUtensorMap &my, const CUtensorMap &mab, const CUtensorMap &mys) {
+        constexpr int NB = 2 + (ACC ? 1 : 0);
+        auto k = vjpk::scan_apply<Op, T, NTC, SC, true, ACC, YS, false, true>;
+        size_t sm = smem_a(NB);
+        set_smem(k, sm);
+        k<<<(unsigned)p.nchunks, NTC, sm, c.stream>>>(ma, my, mab, mys, p);
+        count_launch();
+        return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+    }
+    static vjp_status finish_rs(const ScanCall &c) {
+        Layout L = layout(c.n);
+        const bool acc = (c.flags & VJP_ACCUMULATE) != 0;
+        const bool ys = c.ys != nullptr;
+        {
+            vjpk::ChunkParams pf = cparams(c, L, nchunks_fwd(L));
+            vjpk::scan_tile_prefix<Op, NTC><<<(unsigned)pf.nchunks, NTC, 0, c.stream>>>(pf);
+            count_launch();
+        }
+        const int G = nchunks_for(L, true, acc);
+        vjpk::ChunkParams p = cparams(c, L, G);
+        CUtensorMap ma, my, mab, mys;
+        if (!maps_c(c, p.full_rows, &ma, &my, &mab, &mys)) return VJP_ECUDA;
+        auto kr = vjpk::scan_reduce_rs<Op, T, NTC, SC>;
+        const size_t smr = smem_r(2);
+        set_smem(kr, smr);
+        kr<<<(unsigned)p.nchunks, NTC, smr, c.stream>>>(ma, my, p);
+        count_launch();
+        if (cudaGetLastError() != cudaSuccess) return VJP_ECUDA;
+        if (acc) return ys ? launch_apply_rs<true, true>(c, p, ma, my, mab, mys)
+                           : launch_apply_rs<true, false>(c, p, ma, my, mab, mys);
+        return ys ? launch_apply_rs<false, true>(c, p, ma, my, mab, mys)
+                  : launch_apply_rs<false, false>(c, p, ma, my, mab, mys);
+    }
+
     static vjp_status partial(const ScanCall &c) {
+        if constexpr (Op::kRevNeedsRs) {
+            if (use_rs_chunked(c)) return partial_rs(c);
+        }
         if constexpr (!Op::kRevNeedsRs) {
             if (use_sweep(c)) return partial_sw(c);
             if (use_chunked(c)) return partial_c(c);
@@ -454,6 +513,9 @@ struct ScanImpl {
     }
 
     static vjp_status finish(const ScanCall &c) {
+        if constexpr (Op::kRevNeedsRs) {
+            if (use_rs_chunked(c)) return finish_rs(c);
+        }
         if constexpr (!Op::kRevNeedsRs) {
             if (use_sweep(c)) return finish_sw(c);
             if (use_chunked(c)) return finish_c(c);

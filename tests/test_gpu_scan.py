@@ -63,7 +63,7 @@ def test_scan_parity_sizes(op, dt):
         assert_close(got, ref, dt, what=f"{op} n={n}")
 
 
-@pytest.mark.parametrize("op", ["add", "mul", "linrec", "mat2"])
+@pytest.mark.parametrize("op", ["add", "mul", "min", "max", "linrec", "mat2"])
 def test_scan_parity_lookback_path(op):
     """the single-sweep decoupled look-back kernels (VJP_SCAN_LOOKBACK)"""
     for n in (1, 33, 1023, 4097, 100_003, 1_000_001):
@@ -143,7 +143,7 @@ def test_scan_want_ys(op):
         assert_close(ys.cpu().numpy(), ref_ys, np.float64, what=f"{op} ys n={n}")
 
 
-@pytest.mark.parametrize("op", ["add", "mat2"])
+@pytest.mark.parametrize("op", ["add", "mat2", "max"])
 def test_scan_accumulate(op):
     n = 50_001
     a, yb = make(op, n, np.float64)
@@ -202,3 +202,21 @@ def test_scan_add_2pow30_sampled():
     tail = yb[-100_000:].cpu().numpy()
     ref_tail = oracle.vjp_scan("add", tail, None)
     assert np.array_equal(got[-100_000:].cpu().numpy(), ref_tail)
+
+
+@pytest.mark.parametrize("op", ["min", "max"])
+def test_scan_minmax_special_values(op):
+    """MIN/MAX scans (chunked rs-dependent path): +-inf at the start (the first
+    element's adjoint is rbar_0 whatever a_0 is), long runs of ties
+    (pick-left), -0.0 vs +0.0, a tail spanning tiles; both paths vs the oracle."""
+    n = 300_007
+    k = synth.integers(n, 21, 0, 3)
+    a = (k.to(torch.float64) - 1.5)
+    a[0] = float("inf") if op == "min" else float("-inf")
+    a[1000:1100] = -0.0
+    a[1100:1200] = 0.0
+    yb = synth.uniform(n, 22)
+    ref = oracle.vjp_scan(op, yb.numpy(), a.numpy())
+    for kw in ({}, {"lookback": True}):
+        got = vjp.scan(op, yb.to(DEV), a.to(DEV), **kw).cpu().numpy()
+        assert_close(got, ref, np.float64, what=f"{op} special {kw}")
