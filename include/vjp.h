@@ -161,6 +161,16 @@ vjp_status vjp_scan_partial(vjp_op op, vjp_dtype dtype, int64_t n, const void *a
                             const void *ys_bar, void *ws, size_t ws_bytes,
                             const vjp_shard *shard, void *partial, vjp_stream_t stream,
                             unsigned flags);
+/* MIN/MAX scans need TWO exchanges (their reverse maps depend on the forward
+ * carry): vjp_scan_partial (forward aggregate of the shard) ->
+ * all_gather -> vjp_scan_partial2 (forward prefixes with the shard's forward
+ * carry from gathered1, reverse-map aggregate of the shard -> partial2) ->
+ * all_gather -> vjp_scan_finish with the second gathered array.  Other
+ * operators: VJP_EUNSUPPORTED (one exchange suffices). */
+vjp_status vjp_scan_partial2(vjp_op op, vjp_dtype dtype, int64_t n, const void *as,
+                             const void *ys_bar, void *ws, size_t ws_bytes, const vjp_shard *shard,
+                             const void *gathered1, void *partial2, vjp_stream_t stream,
+                             unsigned flags);
 vjp_status vjp_scan_finish(vjp_op op, vjp_dtype dtype, int64_t n, const void *as,
                            const void *ys_bar, void *as_bar, void *ys, void *ws,
                            size_t ws_bytes, const vjp_shard *shard, const void *gathered,

@@ -65,6 +65,7 @@ def lib():
             "vjp_scan_partial_bytes": ([ci, ci], sz),
             "vjp_scan_partial": ([ci, ci, i64, vp, vp, vp, sz, sp, vp, vp, u32], ci),
             "vjp_scan_finish": ([ci, ci, i64, vp, vp, vp, vp, vp, sz, sp, vp, vp, u32], ci),
+            "vjp_scan_partial2": ([ci, ci, i64, vp, vp, vp, sz, sp, vp, vp, vp, u32], ci),
             "vjp_scan_carries_host": ([ci, ci, ctypes.c_int32, ctypes.c_int32, vp, vp, vp], ci),
             "vjp_reduce_workspace_bytes": ([ci, ci, i64], sz),
             "vjp_reduce": ([ci, ci, i64, vp, vp, vp, vp, vp, vp, sz, vp, u32], ci),

@@ -63,7 +63,6 @@ vjp_status check(const ScanCall &c, bool need_out) {
     disp_for(c.op)(kScanWs, c, &need);
     if (c.ws_bytes < need || (need && !c.ws)) return VJP_EWORKSPACE;
     if (!aligned16(c.ws)) return VJP_EALIGN;
-    if (c.world > 1 && (c.op == VJP_MIN || c.op == VJP_MAX)) return VJP_EUNSUPPORTED;
     // tile count must fit the kernels' 32-bit tile ids
     if (c.n / 1024 > (int64_t)1 << 30) return VJP_EINVAL;
     return VJP_OK;
@@ -162,6 +161,21 @@ vjp_status vjp_scan_partial(vjp_op op, vjp_dtype dtype, int64_t n, const void *a
         return VJP_EUNSUPPORTED;  // empty shards are not supported in the split API
     }
     return disp_for(op)(kScanPartial, c, nullptr);
+}
+
+vjp_status vjp_scan_partial2(vjp_op op, vjp_dtype dtype, int64_t n, const void *as, const void *ys_bar, void *ws,
+                             size_t ws_bytes, const vjp_shard *shard, const void *gathered1, void *partial2,
+                             vjp_stream_t stream, unsigned flags) {
+    if (op != VJP_MIN && op != VJP_MAX) return VJP_EUNSUPPORTED;
+    if (!shard_ok(shard, n) || !shard || shard->world < 2) return VJP_EINVAL;
+    ScanCall c = make_call(op, dtype, n, as, ys_bar, nullptr, nullptr, ws, ws_bytes, stream, flags, shard);
+    c.partial = partial2;
+    c.gathered = gathered1;
+    vjp_status s = check(c, false);
+    if (s != VJP_OK) return s;
+    if (n == 0) return VJP_EUNSUPPORTED;
+    if (!partial2 || !aligned16(partial2) || !gathered1 || !aligned16(gathered1)) return VJP_EINVAL;
+    return disp_for(op)(kScanPartial2, c, nullptr);
 }
 
 vjp_status vjp_scan_finish(vjp_op op, vjp_dtype dtype, int64_t n, const void *as, const void *ys_bar, void *as_bar,

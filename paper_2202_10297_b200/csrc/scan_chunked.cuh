@@ -519,6 +519,29 @@ __global__ void __launch_bounds__(NT, 1) scan_reduce_rs(const __grid_constant__ 
         map_to<Op>(Mc, rec + W);
         st_rec<R>(p.chunkRec + c * R, rec);
     }
+    if (p.partial) {
+        // multi-GPU (second exchange): the last CTA composes the chunk maps, in
+        // chunk order, into the shard record [identity | M_shard]
+        __threadfence();
+        __syncthreads();
+        if (t == 0) sm.last = (atomicAdd(p.counter, 1u) == (unsigned)(p.nchunks - 1));
+        __syncthreads();
+        if (sm.last) {
+            __threadfence();
+            V F;
+            M Mm;
+            range_reduce<Op, NT>(p.chunkRec, 0, p.nchunks, sm.vs, sm.ms, F, Mm);
+            if (t == 0) {
+                double rec[R];
+                const V id = Op::fwd_id();
+#pragma unroll
+                for (int q = 0; q < W; ++q) rec[q] = id.x[q];
+                map_to<Op>(Mm, rec + W);
+                for (int q = 0; q < R; ++q) p.partial[q] = rec[q];
+                *p.counter = 0u;
+            }
+        }
+    }
 }
 
 // =============================================================================

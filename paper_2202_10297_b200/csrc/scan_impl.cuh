@@ -30,7 +30,8 @@ struct ScanCall {
     const void *gathered;  // finish phase: world records (device)
 };
 
-enum ScanPhase { kScanWs = 0, kScanPartial = 1, kScanFinish = 2, kScanPartialBytes = 3, kReduceGeneral = 4 };
+enum ScanPhase { kScanWs = 0, kScanPartial = 1, kScanFinish = 2, kScanPartialBytes = 3, kReduceGeneral = 4,
+                 kScanPartial2 = 5 };
 
 template <class Op, class T>
 struct ScanImpl {
@@ -437,11 +438,15 @@ struct ScanImpl {
     // variant).  Three streaming passes (f64: 8 + 16 + 24 B/elem) instead of the
     // latency-bound single-sweep look-back.  Single GPU.
     static bool use_rs_chunked(const ScanCall &c) {
-        return Op::kRevNeedsRs && c.world == 1 && !(c.flags & VJP_SCAN_LOOKBACK);
+        return Op::kRevNeedsRs && (c.world > 1 || !(c.flags & VJP_SCAN_LOOKBACK));
     }
     static vjp_status partial_rs(const ScanCall &c) {
         Layout L = layout(c.n);
         vjpk::ChunkParams p = cparams(c, L, nchunks_fwd(L));
+        if (c.world > 1) {  // first exchange: the shard's forward aggregate
+            p.partial = static_cast<double *>(c.partial);
+            if (cudaMemsetAsync(p.counter, 0, 4, c.stream) != cudaSuccess) return VJP_ECUDA;
+        }
         CUtensorMap ma, my, mab, mys;
         if (!maps_c(c, p.full_rows, &ma, &my, &mab, &mys)) return VJP_ECUDA;
         auto k = vjpk::scan_reduce<Op, T, NTC, SC, true, false>;
@@ -450,6 +455,38 @@ struct ScanImpl {
         k<<<(unsigned)p.nchunks, NTC, sm, c.stream>>>(ma, my, p);
         count_launch();
         return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+    }
+    // tile prefixes (with the shard forward carry from `gathered` when world > 1)
+    // and K_R' (-> chunk records; world > 1: the shard record for exchange 2)
+    static vjp_status reverse_records_rs(const ScanCall &c, bool acc) {
+        Layout L = layout(c.n);
+        {
+            vjpk::ChunkParams pf = cparams(c, L, nchunks_fwd(L));
+            pf.gathered = static_cast<const double *>(c.gathered);
+            vjpk::scan_tile_prefix<Op, NTC><<<(unsigned)pf.nchunks, NTC, 0, c.stream>>>(pf);
+            count_launch();
+        }
+        const int G = nchunks_for(L, true, acc);
+        vjpk::ChunkParams p = cparams(c, L, G);
+        if (c.world > 1) {
+            p.partial = static_cast<double *>(c.partial);
+            if (cudaMemsetAsync(p.counter, 0, 4, c.stream) != cudaSuccess) return VJP_ECUDA;
+        }
+        CUtensorMap ma, my, mab, mys;
+        if (!maps_c(c, p.full_rows, &ma, &my, &mab, &mys)) return VJP_ECUDA;
+        auto kr = vjpk::scan_reduce_rs<Op, T, NTC, SC>;
+        const size_t smr = smem_r(2);
+        set_smem(kr, smr);
+        kr<<<(unsigned)p.nchunks, NTC, smr, c.stream>>>(ma, my, p);
+        count_launch();
+        return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+    }
+    static vjp_status partial2(const ScanCall &c) {
+        if constexpr (!Op::kRevNeedsRs) {
+            return VJP_EUNSUPPORTED;  // one exchange suffices for these operators
+        } else {
+            return reverse_records_rs(c, (c.flags & VJP_ACCUMULATE) != 0);
+        }
     }
     template <bool ACC, bool YS>
     static vjp_status launch_apply_rs(const ScanCall &c, const vjpk::ChunkParams &p, const CUtensorMap &ma,
@@ -466,21 +503,14 @@ struct ScanImpl {
         Layout L = layout(c.n);
         const bool acc = (c.flags & VJP_ACCUMULATE) != 0;
         const bool ys = c.ys != nullptr;
-        {
-            vjpk::ChunkParams pf = cparams(c, L, nchunks_fwd(L));
-            vjpk::scan_tile_prefix<Op, NTC><<<(unsigned)pf.nchunks, NTC, 0, c.stream>>>(pf);
-            count_launch();
-        }
+        if (c.world == 1) {
+            vjp_status st = reverse_records_rs(c, acc);
+            if (st != VJP_OK) return st;
+        }  // world > 1: done by vjp_scan_partial2 before the second exchange
         const int G = nchunks_for(L, true, acc);
         vjpk::ChunkParams p = cparams(c, L, G);
         CUtensorMap ma, my, mab, mys;
         if (!maps_c(c, p.full_rows, &ma, &my, &mab, &mys)) return VJP_ECUDA;
-        auto kr = vjpk::scan_reduce_rs<Op, T, NTC, SC>;
-        const size_t smr = smem_r(2);
-        set_smem(kr, smr);
-        kr<<<(unsigned)p.nchunks, NTC, smr, c.stream>>>(ma, my, p);
-        count_launch();
-        if (cudaGetLastError() != cudaSuccess) return VJP_ECUDA;
         if (acc) return ys ? launch_apply_rs<true, true>(c, p, ma, my, mab, mys)
                            : launch_apply_rs<true, false>(c, p, ma, my, mab, mys);
         return ys ? launch_apply_rs<false, true>(c, p, ma, my, mab, mys)
@@ -559,11 +589,13 @@ vjp_status scan_dispatch(int phase, const ScanCall &c, size_t *out) {
         using I = ScanImpl<Op, double>;
         if (phase == kScanWs) { *out = I::layout(c.n).total; return VJP_OK; }
         if (phase == kReduceGeneral) return I::reduce_general(c);
+        if (phase == kScanPartial2) return I::partial2(c);
         return phase == kScanPartial ? I::partial(c) : I::finish(c);
     }
     using I = ScanImpl<Op, float>;
     if (phase == kScanWs) { *out = I::layout(c.n).total; return VJP_OK; }
     if (phase == kReduceGeneral) return I::reduce_general(c);
+    if (phase == kScanPartial2) return I::partial2(c);
     return phase == kScanPartial ? I::partial(c) : I::finish(c);
 }
 

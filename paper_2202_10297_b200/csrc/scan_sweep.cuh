@@ -136,7 +136,12 @@ __global__ void __launch_bounds__(NT) scan_tile_prefix(const ChunkParams p) {
             f = Op::fwd(f, v);
         }
     }
-    const V Fpre = block_reduce_fwd<Op, NW>(f, vs);
+    V Fpre = block_reduce_fwd<Op, NW>(f, vs);
+    if (p.world > 1 && p.gathered) {  // multi-GPU (MIN/MAX split): the shards to the left come first
+        V Fsh, Hunused;
+        shard_carries<Op>(p.gathered, p.rank, p.world, Fsh, Hunused);
+        Fpre = Op::fwd(Fsh, Fpre);
+    }
     const int64_t per = (k + NT - 1) / NT;
     f = Op::fwd_id();
     for (int64_t j = t0 + t * per; j < t0 + (t + 1) * per && j < t1; ++j) {

@@ -7,6 +7,8 @@ exchange step:
   scan            partial (forward re-execution + reverse-map aggregate of the
                   shard) -> all_gather of the per-shard records (40 B LINREC,
                   96 B MAT2) -> finish (return sweep with the combined carries).
+                  MIN/MAX: two exchanges (forward aggregates, then reverse
+                  aggregates built with the forward carry: partial2).
   reduce          partial record (p, z, i0) / (value, index) / sum -> all_gather
                   -> finish (deterministic rank-order combine on the device).
   reduce_by_index per-bin state -> all_reduce (PRODUCT+SUM for *, MAX/MIN then
@@ -25,7 +27,7 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-from . import (ACCUMULATE, WIDTH, VjpShard, _check, _dt, _it, _op, _p, _stream, lib, workspace)
+from . import (ACCUMULATE, MAX, MIN, WIDTH, VjpShard, _check, _dt, _it, _op, _p, _stream, lib, workspace)
 
 
 def _all_gather_into(out: torch.Tensor, inp: torch.Tensor, group=None):
@@ -90,6 +92,12 @@ def scan(op, ys_bar: torch.Tensor, as_: torch.Tensor | None, *, offset: int, glo
     if world > 1:
         gathered = torch.empty(world * rec, dtype=torch.float64, device=dev)
         _all_gather_into(gathered, part, group)
+        if o in (MIN, MAX):  # rs-dependent maps: a second exchange of reverse aggregates
+            part2 = torch.empty(rec, dtype=torch.float64, device=dev)
+            _check(L.vjp_scan_partial2(o, dt, n, _p(as_), _p(ys_bar), _p(ws), nbytes, sh, _p(gathered), _p(part2), s,
+                                       flags), "vjp_scan_partial2")
+            gathered = torch.empty(world * rec, dtype=torch.float64, device=dev)
+            _all_gather_into(gathered, part2, group)
     if events:
         events["finish_start"].record()
     _check(L.vjp_scan_finish(o, dt, n, _p(as_), _p(ys_bar), _p(ab), _p(ys), _p(ws), nbytes, sh, _p(gathered), s,

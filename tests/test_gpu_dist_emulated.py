@@ -74,6 +74,45 @@ def test_scan_split_emulated(op, world):
     assert_close(got, ref, np.float64, what=f"split {op} world={world}")
 
 
+@pytest.mark.parametrize("world", [2, 3, 5])
+@pytest.mark.parametrize("op", ["min", "max"])
+def test_scan_minmax_two_exchanges_emulated(op, world):
+    """MIN/MAX scans across shards: partial (forward aggregates) -> gather ->
+    partial2 (reverse aggregates with the shard forward carry) -> gather ->
+    finish; many exact ties (pick-left) so the forward carry decides sides."""
+    L = vjp.lib()
+    o = vjp.OPS[op]
+    N = 200_003
+    k = synth.integers(N, 9, 0, 63)
+    a = k.to(torch.float64) / 64.0
+    yb = synth.uniform(N, 10)
+    ref = oracle.vjp_scan(op, yb.numpy(), a.numpy())
+    rec = L.vjp_scan_partial_bytes(o, 2) // 8
+    state, parts = [], []
+    for r, (off, n) in enumerate(shards(N, world)):
+        a_r = a[off:off + n].clone().to(DEV)
+        y_r = yb[off:off + n].clone().to(DEV)
+        ws = torch.empty(L.vjp_scan_workspace_bytes(o, 2, n), dtype=torch.uint8, device=DEV)
+        part = torch.empty(rec, dtype=torch.float64, device=DEV)
+        sh = VjpShard(r, world, off, N)
+        assert L.vjp_scan_partial(o, 2, n, _p(a_r), _p(y_r), _p(ws), ws.numel(), sh, _p(part), _s(), 0) == 0
+        parts.append(part)
+        state.append((a_r, y_r, ws, sh, n))
+    g1 = torch.cat(parts)
+    parts2 = []
+    for a_r, y_r, ws, sh, n in state:
+        part2 = torch.empty(rec, dtype=torch.float64, device=DEV)
+        assert L.vjp_scan_partial2(o, 2, n, _p(a_r), _p(y_r), _p(ws), ws.numel(), sh, _p(g1), _p(part2), _s(), 0) == 0
+        parts2.append(part2)
+    g2 = torch.cat(parts2)
+    outs = []
+    for a_r, y_r, ws, sh, n in state:
+        ab = torch.empty_like(y_r)
+        assert L.vjp_scan_finish(o, 2, n, _p(a_r), _p(y_r), _p(ab), None, _p(ws), ws.numel(), sh, _p(g2), _s(), 0) == 0
+        outs.append(ab)
+    assert_close(torch.cat(outs).cpu().numpy(), ref, np.float64, what=f"split {op} world={world}")
+
+
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("op,zeros", [("add", "none"), ("mul", "none"), ("mul", "one"), ("mul", "two"),
                                       ("min", None), ("max", None)])

@@ -42,11 +42,14 @@ def _worker(rank, world, port, q):
         results = {}
         # scan LINREC / MAT2 / ADD over a global array split in contiguous shards
         for op, gen, w in (("linrec", synth.linrec_inputs, 2), ("mat2", synth.mat2_inputs, 4),
-                           ("add", None, 1)):
+                           ("add", None, 1), ("min", "min", 1)):
             N = 300_007
             off, n = vdist.shard_bounds(N, world, rank)
             if gen is None:
                 a_l, y_l = None, synth.scan_add_seed(n, offset=off, device=dev)
+            elif gen == "min":  # two exchanges (rs-dependent reverse maps)
+                a_l = synth.integers(n, 9, 0, 63, offset=off, device=dev).to(torch.float64) / 64.0
+                y_l = synth.uniform(n, 10, offset=off, device=dev)
             else:
                 a_l, y_l = gen(n, offset=off, device=dev)
             ab = vdist.scan(op, y_l, a_l, offset=off, global_n=N)
@@ -55,6 +58,8 @@ def _worker(rank, world, port, q):
             if rank == 0:
                 if gen is None:
                     a, y = None, synth.scan_add_seed(N)
+                elif gen == "min":
+                    a, y = synth.integers(N, 9, 0, 63).to(torch.float64) / 64.0, synth.uniform(N, 10)
                 else:
                     a, y = gen(N)
                 ref = oracle.vjp_scan(op, y.numpy(), None if a is None else a.numpy())
