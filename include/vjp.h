@@ -315,8 +315,8 @@ vjp_status vjp_debug_log2_abs(const double *x, double *y, int64_t n, vjp_stream_
  * sweep is computed per component exactly as vjp_scan (the vectorised plus
  * case, is the per-column reversed suffix sum).
  *   as [n][width][W] (NULL allowed for ADD); ys_bar, as_bar likewise.
- * VJP_ACCUMULATE: as_bar += .  MIN/MAX -> VJP_EUNSUPPORTED (their reverse maps
- * need the forward carry; use vjp_scan per component).  Errors: VJP_EINVAL,
+ * VJP_ACCUMULATE: as_bar += .  MIN/MAX (pick-left subgradient) take two more
+ * passes (their reverse maps need the forward carry).  Errors: VJP_EINVAL,
  * VJP_EALIGN, VJP_EWORKSPACE, VJP_ECUDA.
  * ==================================================================== */
 size_t vjp_scan_batched_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_t n, int64_t width);

@@ -21,9 +21,9 @@
 //        hold the tile's rows, the primal is re-executed from the tile prefix
 //        (tape-free), outputs run right to left:
 //        rbar_i = ybar_i + H, abar_i = J_R^T rbar_i, H = J_L^T rbar_i.
-// Operators with carry-independent reverse maps (ADD, MUL, LINREC, MAT2); the
-// MIN/MAX scans need the forward carry inside the reverse maps and are not
-// offered batched (VJP_EUNSUPPORTED).
+// ADD, MUL, LINREC, MAT2 (carry-independent reverse maps) and MIN/MAX, whose
+// reverse maps need the forward carry: forward records, forward prefixes,
+// maps rebuilt with the true rs (scan_bat_maps_rs), then the carries.
 #include <cstdint>
 #include <type_traits>
 
@@ -67,7 +67,7 @@ __device__ __forceinline__ bool bat_coord(const BatParams &p, int64_t &c, int64_
     return j < p.w && c < p.C;
 }
 
-template <class Op, class T, bool FWD>
+template <class Op, class T, bool FWD, bool MAPS = true>
 __global__ void __launch_bounds__(kBatThreads) scan_bat_reduce(const BatParams p) {
     using V = typename Op::Val;
     using M = typename Op::Map;
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(kBatThreads) scan_bat_reduce(const BatParams p
         for (int r = 0; r < TR; ++r) {
             if (rt + r < p.n) {
                 if (FWD) F = Op::fwd(F, a[r]);
-                Mc = Op::compose(Mc, Op::make_map(Op::fwd_id(), a[r], y[r]));
+                if (MAPS) Mc = Op::compose(Mc, Op::make_map(Op::fwd_id(), a[r], y[r]));
             }
         }
     }
@@ -113,6 +113,49 @@ __global__ void __launch_bounds__(kBatThreads) scan_bat_reduce(const BatParams p
     double *dst = p.rec + (c * p.w + j) * (W + MD);
 #pragma unroll
     for (int q = 0; q < W + MD; ++q) dst[q] = rec[q];
+}
+
+// rs-dependent operators (MIN/MAX): the chunk's reverse map with the TRUE rs,
+// walking the rows from the chunk's forward prefix (carry[..][0..W), written
+// by a first scan_bat_carries); only the M part of the record is rewritten
+template <class Op, class T>
+__global__ void __launch_bounds__(kBatThreads) scan_bat_maps_rs(const BatParams p) {
+    using V = typename Op::Val;
+    using M = typename Op::Map;
+    constexpr int W = Op::W, MD = Op::kMapD, TR = BatGeo<Op>::TR;
+    int64_t c, j;
+    if (!bat_coord(p, c, j)) return;
+    const T *as = static_cast<const T *>(p.as);
+    const T *yb = static_cast<const T *>(p.ys_bar);
+    const double *cr = p.carry + (c * p.w + j) * 2 * W;
+    V rs;
+#pragma unroll
+    for (int q = 0; q < W; ++q) rs.x[q] = cr[q];
+    M Mc = Op::map_id();
+    const int64_t r0 = c * p.TPC * TR, r1 = r0 + p.TPC * TR < p.n ? r0 + p.TPC * TR : p.n;
+    for (int64_t rt = r0; rt < r1; rt += TR) {
+        V a[TR], y[TR];
+#pragma unroll
+        for (int r = 0; r < TR; ++r) {
+            if (rt + r < r1) {
+                const int64_t e = ((rt + r) * p.w + j) * W;
+                a[r] = bat_ld<T, W>(as + e);
+                y[r] = bat_ld<T, W>(yb + e);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < TR; ++r) {
+            if (rt + r < r1) {
+                Mc = Op::compose(Mc, Op::make_map(rs, a[r], y[r]));
+                rs = Op::fwd(rs, a[r]);
+            }
+        }
+    }
+    double rec[MD];
+    map_to<Op>(Mc, rec);
+    double *dst = p.rec + (c * p.w + j) * (W + MD) + W;
+#pragma unroll
+    for (int q = 0; q < MD; ++q) dst[q] = rec[q];
 }
 
 // one CTA (256 threads) per column: exclusive scans over the C chunk records
@@ -218,6 +261,7 @@ __global__ void __launch_bounds__(kBatThreads) scan_bat_apply(const BatParams p)
 #pragma unroll
             for (int q = 0; q < W; ++q) g.x[q] = y[r].x[q] + X.x[q];  // rbar_i = ybar_i + H_{i+1}
             V o = Op::out(rsp[r], a[r], g);
+            if (Op::kFirstSpecial && rt + r == 0) o = g;  // abar_0 = rbar_0, whatever a_0 is
             X = Op::pass_left(rsp[r], a[r], g);
             T *dst = ab + ((rt + r) * p.w + j) * W;
 #pragma unroll
@@ -283,7 +327,16 @@ vjp_status bat_run(int64_t n, int64_t w, const void *as, const void *yb, void *a
     constexpr bool FWD = !std::is_same<Op, vjpk::OpAdd>::value;
     const dim3 grid((unsigned)((w + L.CW - 1) / L.CW), (unsigned)((L.C + L.CPB - 1) / L.CPB));
     if (grid.y > 65535u) return VJP_EUNSUPPORTED;
-    vjpk::scan_bat_reduce<Op, T, FWD><<<grid, vjpk::kBatThreads, 0, s>>>(p);
+    if constexpr (Op::kRevNeedsRs) {
+        // MIN/MAX: forward records -> forward prefixes -> maps with the true rs
+        // -> carries again (forward prefixes recomputed identically, reverse now valid)
+        vjpk::scan_bat_reduce<Op, T, true, false><<<grid, vjpk::kBatThreads, 0, s>>>(p);
+        vjpk::scan_bat_carries<Op><<<(unsigned)w, 256, 0, s>>>(p);
+        vjpk::scan_bat_maps_rs<Op, T><<<grid, vjpk::kBatThreads, 0, s>>>(p);
+        count_launch(2);
+    } else {
+        vjpk::scan_bat_reduce<Op, T, FWD><<<grid, vjpk::kBatThreads, 0, s>>>(p);
+    }
     vjpk::scan_bat_carries<Op><<<(unsigned)w, 256, 0, s>>>(p);
     if (p.acc)
         vjpk::scan_bat_apply<Op, T, FWD, true><<<grid, vjpk::kBatThreads, 0, s>>>(p);
@@ -306,6 +359,8 @@ size_t vjp_scan_batched_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_t n, i
     case VJP_MUL: return bat_ws<vjpk::OpMul>(n, width);
     case VJP_LINREC: return bat_ws<vjpk::OpLinrec>(n, width);
     case VJP_MAT2: return bat_ws<vjpk::OpMat2>(n, width);
+    case VJP_MIN: return bat_ws<vjpk::OpMin>(n, width);
+    case VJP_MAX: return bat_ws<vjpk::OpMax>(n, width);
     default: return 0;
     }
 }
@@ -314,8 +369,7 @@ vjp_status vjp_scan_batched(vjp_op op, vjp_dtype dtype, int64_t n, int64_t width
                             const void *ys_bar, void *as_bar, void *ws, size_t ws_bytes, vjp_stream_t stream,
                             unsigned flags) {
     if ((dtype != VJP_F32 && dtype != VJP_F64) || n < 0 || width < 1) return VJP_EINVAL;
-    if (op == VJP_MIN || op == VJP_MAX) return VJP_EUNSUPPORTED;
-    if (op != VJP_ADD && op != VJP_MUL && op != VJP_LINREC && op != VJP_MAT2) return VJP_EINVAL;
+    if (op < VJP_ADD || op > VJP_MAT2) return VJP_EINVAL;
     if (n == 0) return VJP_OK;
     if (!ys_bar || !as_bar || (op != VJP_ADD && !as)) return VJP_EINVAL;
     if (as_bar == ys_bar || (as && as_bar == as)) return VJP_EINVAL;
@@ -337,6 +391,12 @@ vjp_status vjp_scan_batched(vjp_op op, vjp_dtype dtype, int64_t n, int64_t width
     case VJP_LINREC:
         return f64 ? bat_run<vjpk::OpLinrec, double>(n, width, as, ys_bar, as_bar, ws, s, flags)
                    : bat_run<vjpk::OpLinrec, float>(n, width, as, ys_bar, as_bar, ws, s, flags);
+    case VJP_MIN:
+        return f64 ? bat_run<vjpk::OpMin, double>(n, width, as, ys_bar, as_bar, ws, s, flags)
+                   : bat_run<vjpk::OpMin, float>(n, width, as, ys_bar, as_bar, ws, s, flags);
+    case VJP_MAX:
+        return f64 ? bat_run<vjpk::OpMax, double>(n, width, as, ys_bar, as_bar, ws, s, flags)
+                   : bat_run<vjpk::OpMax, float>(n, width, as, ys_bar, as_bar, ws, s, flags);
     default:
         return f64 ? bat_run<vjpk::OpMat2, double>(n, width, as, ys_bar, as_bar, ws, s, flags)
                    : bat_run<vjpk::OpMat2, float>(n, width, as, ys_bar, as_bar, ws, s, flags);

@@ -59,10 +59,18 @@ def test_batched_add_integer_bit_exact_and_accumulate():
     assert_close(out.cpu().numpy(), ref, np.float64, what="batched accumulate")
 
 
-def test_batched_minmax_unsupported():
-    yb = torch.ones(100, dtype=torch.float64, device=DEV)
-    with pytest.raises(vjp.VjpError):
-        vjp.scan_batched("min", yb, yb.clone(), width=4)
+@pytest.mark.parametrize("op", ["min", "max"])
+def test_batched_minmax(op):
+    """MIN/MAX vectorised scans (pick-left ties, +-inf first row) vs the
+    oracle's transpose rule over the sequential scalar scans."""
+    for n, w in ((1, 1), (777, 33), (4097, 7), (100_003, 16), (20, 5000)):
+        k = synth.integers(n * w, 9, 0, 15)
+        a = k.to(torch.float64) / 16.0
+        a[:w] = float("inf") if op == "min" else float("-inf")
+        yb = synth.uniform(n * w, 10)
+        ref = oracle.vjp_scan_batched(op, yb.numpy(), a.numpy(), w)
+        got = vjp.scan_batched(op, yb.to(DEV), a.to(DEV), width=w).cpu().numpy()
+        assert_close(got, ref, np.float64, what=f"batched {op} n={n} w={w}")
 
 
 def test_batched_empty():
