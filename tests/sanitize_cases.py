@@ -31,6 +31,17 @@ for op in ('add', 'mul', 'min', 'max'):
 is_, yb = synth.scatter_inputs(10_000, 3000, device=dev)
 vjp.scatter(is_, yb)
 vjp.scatter(is_, yb.clone(), in_place=True)
+for op in ('linrec', 'mat2'):  # general reduce rule (YL kernels)
+    w = vjp.WIDTH[vjp.OPS[op]]
+    for n in (1, 1000, 70_001):
+        a = 0.5 + synth.uniform(n * w, 1, device=dev)
+        vjp.reduce(op, a, torch.ones(w, dtype=torch.float64, device=dev), want_y=True)
+for op in ('add', 'mul', 'min', 'max', 'linrec', 'mat2'):  # vectorised scans
+    w = vjp.WIDTH[vjp.OPS[op]]
+    for n, width in ((5, 3), (777, 33), (3001, 2)):
+        a = 0.5 + synth.uniform(n * width * w, 1, device=dev)
+        yb = synth.uniform(n * width * w, 2, device=dev)
+        vjp.scan_batched(op, yb, None if op == 'add' else a, width=width)
 for n, k, d in ((1, 1, 1), (129, 65, 17), (5000, 100, 64), (3000, 20, 70)):  # config-5 composite
     for dt in (torch.float64, torch.float32):
         P, C = synth.kmeans_inputs(n, k, d, dtype=dt, device=dev)
