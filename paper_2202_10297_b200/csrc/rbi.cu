@@ -25,6 +25,14 @@
 namespace vjpk {
 
 constexpr int kBThreads = 256;
+// shared-memory histogram kernels (MIN/MAX phase A, small-m MUL): <= 64
+// registers -> 4 CTAs (32 warps) per SM to hide the load latency (78 registers
+// gave 3 CTAs, long-scoreboard bound): MAX m=1e3 1.21 -> 1.11 ms.  Measured
+// slower for the gather / L2-reduction kernels, which keep their registers.
+#ifndef VJP_RBI_MINB
+#define VJP_RBI_MINB 4
+#endif
+constexpr int kBMinBlocks = VJP_RBI_MINB;
 
 template <class I>
 struct IdxVec;
@@ -282,7 +290,7 @@ __global__ void __launch_bounds__(kBThreads) rbi_fwd_log(const I *__restrict__ i
 // owner-table conflict resolution: 2.42 vs 2.72 ms at m = 10^3, and it keeps
 // full occupancy at larger m)
 template <class T, class I>
-__global__ void __launch_bounds__(kBThreads) rbi_fwd_smem_log(const I *__restrict__ inds, const T *__restrict__ as,
+__global__ void __launch_bounds__(kBThreads, kBMinBlocks) rbi_fwd_smem_log(const I *__restrict__ inds, const T *__restrict__ as,
                                                               RbiParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     double *lg = reinterpret_cast<double *>(smem);
@@ -330,7 +338,7 @@ __device__ __forceinline__ void red_max_u64_shared(unsigned long long *a, unsign
 // key).  SMEM (small m): the filter is a per-CTA shared-memory table merged
 // into the global keys at the end; large m: the global keys in L2.
 template <class T, class I, int OP, bool SMEM>
-__global__ void __launch_bounds__(kBThreads) rbi_ext_a(const I *__restrict__ inds, const T *__restrict__ as,
+__global__ void __launch_bounds__(kBThreads, kBMinBlocks) rbi_ext_a(const I *__restrict__ inds, const T *__restrict__ as,
                                                        RbiParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long *hk = reinterpret_cast<unsigned long long *>(smem);
