@@ -175,8 +175,10 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (synth/, seed 2202)",
-        "config": {"workload": "vjp_scan LINREC+MAT2 f64 (bounded sample: n=2^22 per op per step)",
-                   "n_per_op": n, "ops": ["linrec", "mat2"], "parallelism": "1 CPU thread"},
+        "config": {"workload": "configs[1]: vjp_scan LINREC + MAT2, n = 2^26 elements per op per GPU, f64",
+                   "ops": ["linrec", "mat2"], "parallelism": "1 CPU thread (the oracle)",
+                   "sample": f"bounded: each step runs n = 2^22 elements per op ({n} of the 2^26), "
+                             "the metric is per element so it is comparable"},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
                          "sample": f"LINREC+MAT2 n=2^22 each per step, {args.steps} steps"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
