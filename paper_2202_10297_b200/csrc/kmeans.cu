@@ -245,11 +245,13 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
                  : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
 }
 
+constexpr int KM_MMA_NT = 256;  // 8 warps: 4 point groups x 2 center halves
+
 template <class T, bool RES>
-__global__ void __launch_bounds__(KM_NT, 2) km_assign_mma(const T *__restrict__ P, const T *__restrict__ C,
-                                                          const double *__restrict__ cn, int64_t n, int64_t k,
-                                                          int64_t d, int32_t *__restrict__ assign,
-                                                          double *__restrict__ cost_part) {
+__global__ void __launch_bounds__(KM_MMA_NT, 2) km_assign_mma(const T *__restrict__ P, const T *__restrict__ C,
+                                                              const double *__restrict__ cn, int64_t n, int64_t k,
+                                                              int64_t d, int32_t *__restrict__ assign,
+                                                              double *__restrict__ cost_part) {
     extern __shared__ __align__(16) double km_smem[];
     const int nd = (int)((d + KM_KD - 1) / KM_KD);
     const int PW = (RES ? nd * KM_KD : KM_KD) + KM_PS_PAD;  // P row stride (doubles)
@@ -257,6 +259,7 @@ __global__ void __launch_bounds__(KM_NT, 2) km_assign_mma(const T *__restrict__ 
     double *Ps = km_smem;                                    // RES: [128][PW]; else [2][128][PW]
     double *Cs = km_smem + (size_t)(RES ? 1 : 2) * KM_BP * PW;  // [2][64][CW]
     const int t = threadIdx.x, lane = t & 31, w = t >> 5, g = lane >> 2, tig = lane & 3;
+    const int pg = w >> 1, ch = w & 1;  // warp: points [32 pg, 32 pg + 32) x centers [32 ch, 32 ch + 32) of the tile
     const int64_t p0 = (int64_t)blockIdx.x * KM_BP;
     const int nct = (int)((k + KM_BC - 1) / KM_BC), nst = nct * nd;
 
@@ -264,8 +267,8 @@ __global__ void __launch_bounds__(KM_NT, 2) km_assign_mma(const T *__restrict__ 
         const int ct = st / nd, dc = st % nd, buf = st & 1;
         const int64_t c0 = (int64_t)ct * KM_BC, d0 = (int64_t)dc * KM_KD;
         double *cs = Cs + (size_t)buf * KM_BC * CW;
-#pragma unroll 4
-        for (int idx = t; idx < KM_BC * KM_KD; idx += KM_NT) {
+#pragma unroll 2
+        for (int idx = t; idx < KM_BC * KM_KD; idx += KM_MMA_NT) {
             const int cc = idx / KM_KD, kk = idx % KM_KD;
             const int64_t gc = c0 + cc, gd = d0 + kk;
             const bool ok = gc < k && gd < d;
@@ -273,8 +276,8 @@ __global__ void __launch_bounds__(KM_NT, 2) km_assign_mma(const T *__restrict__ 
         }
         if (!RES) {
             double *ps = Ps + (size_t)buf * KM_BP * PW;
-#pragma unroll 4
-            for (int idx = t; idx < KM_BP * KM_KD; idx += KM_NT) {
+#pragma unroll 2
+            for (int idx = t; idx < KM_BP * KM_KD; idx += KM_MMA_NT) {
                 const int pp = idx / KM_KD, kk = idx % KM_KD;
                 const int64_t gp = p0 + pp, gd = d0 + kk;
                 const bool ok = gp < n && gd < d;
@@ -286,7 +289,7 @@ __global__ void __launch_bounds__(KM_NT, 2) km_assign_mma(const T *__restrict__ 
     if (RES) {
         const int DP = nd * KM_KD;
 #pragma unroll 4
-        for (int idx = t; idx < KM_BP * DP; idx += KM_NT) {
+        for (int idx = t; idx < KM_BP * DP; idx += KM_MMA_NT) {
             const int pp = idx / DP, kk = idx % DP;
             const int64_t gp = p0 + pp;
             const bool ok = gp < n && kk < d;
@@ -302,15 +305,15 @@ __global__ void __launch_bounds__(KM_NT, 2) km_assign_mma(const T *__restrict__ 
         bv[i] = INFINITY;
         bj[i] = 0x7fffffff;
     }
-    double pnorm = 0.0;
-    double acc[4][8][2];
+    double pnorm = 0.0;  // threads t < 128: ||p_{p0 + t}||^2
+    double acc[4][4][2];
     for (int st = 0; st < nst; ++st) {
         const int ct = st / nd, dc = st % nd;
         if (dc == 0) {
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+                for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
         }
         if (st + 1 < nst) {
             __syncthreads();
@@ -322,29 +325,29 @@ __global__ void __launch_bounds__(KM_NT, 2) km_assign_mma(const T *__restrict__ 
         __syncthreads();
         const double *ps = RES ? Ps + dc * KM_KD : Ps + (size_t)(st & 1) * KM_BP * PW;
         const double *cs = Cs + (size_t)(st & 1) * KM_BC * CW;
-        if (ct == 0) {
+        if (ct == 0 && t < KM_BP) {
 #pragma unroll 8
             for (int kk = 0; kk < KM_KD; ++kk) {
                 const double v = ps[t * PW + kk];
                 pnorm = fma(v, v, pnorm);
             }
         }
-#pragma unroll 2
+#pragma unroll 4
         for (int k4 = 0; k4 < KM_KD; k4 += 4) {
-            double a[4], b[8];
+            double a[4], b[4];
 #pragma unroll
-            for (int mi = 0; mi < 4; ++mi) a[mi] = ps[(w * 32 + mi * 8 + g) * PW + k4 + tig];
+            for (int mi = 0; mi < 4; ++mi) a[mi] = ps[(pg * 32 + mi * 8 + g) * PW + k4 + tig];
 #pragma unroll
-            for (int ni = 0; ni < 8; ++ni) b[ni] = cs[(ni * 8 + g) * CW + k4 + tig];
+            for (int ni = 0; ni < 4; ++ni) b[ni] = cs[(ch * 32 + ni * 8 + g) * CW + k4 + tig];
 #pragma unroll
             for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-                for (int ni = 0; ni < 8; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+                for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
         }
         if (dc == nd - 1) {
-            const int64_t c0 = (int64_t)ct * KM_BC;
+            const int64_t c0 = (int64_t)ct * KM_BC + ch * 32;
 #pragma unroll
-            for (int ni = 0; ni < 8; ++ni)
+            for (int ni = 0; ni < 4; ++ni)
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
                     const int64_t gc = c0 + ni * 8 + tig * 2 + e;
@@ -375,25 +378,39 @@ __global__ void __launch_bounds__(KM_NT, 2) km_assign_mma(const T *__restrict__ 
             }
         }
     __syncthreads();
-    double *pn = Cs;          // [128] ||p||^2
-    double *mv = Cs + KM_BP;  // [128] min candidate
-    pn[t] = pnorm;
+    double *pn = Cs;                                                    // [128]
+    double *hv = Cs + KM_BP;                                            // [2][128] per center half
+    int32_t *hj = reinterpret_cast<int32_t *>(Cs + 3 * KM_BP);          // [2][128]
+    if (t < KM_BP) pn[t] = pnorm;
     if (tig == 0) {
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi) {
-            const int pp = w * 32 + mi * 8 + g;
-            mv[pp] = bv[mi];
-            const int64_t gp = p0 + pp;
-            if (gp < n) assign[gp] = bj[mi];
+            const int pp = pg * 32 + mi * 8 + g;
+            hv[ch * KM_BP + pp] = bv[mi];
+            hj[ch * KM_BP + pp] = bj[mi];
         }
     }
     __syncthreads();
-    double md = (p0 + t < n) ? fmax(pn[t] + mv[t], 0.0) : 0.0;
+    double md = 0.0;
+    if (t < KM_BP) {
+        double v = hv[t];
+        int32_t j = hj[t];
+        const double v1 = hv[KM_BP + t];
+        const int32_t j1 = hj[KM_BP + t];
+        if (v1 < v || (v1 == v && j1 < j)) {
+            v = v1;
+            j = j1;
+        }
+        if (p0 + t < n) {
+            assign[p0 + t] = j;
+            md = fmax(pn[t] + v, 0.0);
+        }
+    }
     for (int o = 16; o > 0; o >>= 1) md += __shfl_down_sync(0xffffffffu, md, o);
     __syncthreads();
-    if (lane == 0) mv[w] = md;
+    if (lane == 0 && w < 4) hv[w] = md;
     __syncthreads();
-    if (t == 0) cost_part[blockIdx.x] = ((mv[0] + mv[1]) + mv[2]) + mv[3];
+    if (t == 0) cost_part[blockIdx.x] = ((hv[0] + hv[1]) + hv[2]) + hv[3];
 }
 
 __global__ void km_hist(const int32_t *__restrict__ assign, int64_t n, int64_t k, int32_t *__restrict__ hist) {
@@ -640,7 +657,7 @@ vjp_status km_run(int64_t n, int64_t k, int64_t d, const void *P, const void *C,
                                 (size_t)2 * vjpk::KM_BC * (vjpk::KM_KD + vjpk::KM_PS_PAD)) * 8;
             auto km = res ? vjpk::km_assign_mma<T, true> : vjpk::km_assign_mma<T, false>;
             cudaFuncSetAttribute(km, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm);
-            km<<<(unsigned)L.nbA, vjpk::KM_NT, msm, s>>>(Pt, Ct, cn, n, k, d, asg, part);
+            km<<<(unsigned)L.nbA, vjpk::KM_MMA_NT, msm, s>>>(Pt, Ct, cn, n, k, d, asg, part);
         } else {
             auto ka = res ? vjpk::km_assign<T, true> : vjpk::km_assign<T, false>;
             cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asm_);
