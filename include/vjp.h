@@ -91,10 +91,11 @@ enum {
     VJP_SCAN_LOOKBACK = 1u << 16, /* tuning/testing: vjp_scan uses the single-sweep decoupled
                                     look-back kernels instead of the chunked reduce-then-scan
                                     kernels (MIN/MAX always use look-back) */
-    VJP_SCAN_SWEEP = 1u << 17     /* tuning/testing (single GPU, ADD/MUL/LINREC/MAT2): one
-                                    persistent kernel that reads as/ys_bar from HBM once and
-                                    re-reads each round from L2 (method bytes); slower than the
-                                    default chunked kernels on B200 */
+    VJP_SCAN_SWEEP = 1u << 17,    /* single GPU: the one-read L2-round sweep (one persistent
+                                    kernel, as/ys_bar read from HBM once, each round re-read
+                                    from L2) for any of ADD/MUL/LINREC/MAT2; it is already the
+                                    default for ADD without ys */
+    VJP_SCAN_CHUNKED = 1u << 18   /* tuning/testing: force the two chunked kernels */
 };
 
 /* One shard of a multi-GPU call: this process owns global elements

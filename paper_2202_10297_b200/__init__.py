@@ -29,6 +29,7 @@ ACCUMULATE = 1
 CHECK_INDICES = 2
 SCAN_LOOKBACK = 1 << 16
 SCAN_SWEEP = 1 << 17
+SCAN_CHUNKED = 1 << 18
 STATUS = {0: "VJP_OK", 1: "VJP_EINVAL", 2: "VJP_EUNSUPPORTED", 3: "VJP_EWORKSPACE", 4: "VJP_ECUDA",
           5: "VJP_EDUPINDEX", 6: "VJP_EOOB", 7: "VJP_EALIGN"}
 
@@ -186,15 +187,15 @@ def _host_out(t: torch.Tensor, like_host: bool):
 # ----------------------------------------------------------------- calls
 
 def scan(op, ys_bar: torch.Tensor, as_: torch.Tensor | None = None, *, out: torch.Tensor | None = None,
-         want_ys: bool = False, accumulate: bool = False, lookback: bool = False, sweep: bool = False):
+         want_ys: bool = False, accumulate: bool = False, lookback: bool = False, sweep: bool = False, chunked: bool = False):
     """as_bar of ``ys = scan op as_`` with output adjoint ``ys_bar`` (sec 5.2).
 
     Tensors hold n elements of the operator's width (LINREC: (d, c) pairs,
     MAT2: row-major 2x2), any shape with that many scalars.  Returns as_bar
     (same shape as ys_bar), or (as_bar, ys) if want_ys.  lookback=True selects
     the single-sweep decoupled look-back kernels, sweep=True the one-read
-    L2-round sweep (both tuning/testing; the default is the chunked
-    reduce-then-scan)."""
+    L2-round sweep, chunked=True the two chunked kernels (tuning/testing; the
+    default is the sweep for scan(+) and the chunked kernels otherwise)."""
     o = _op(op)
     host = not ys_bar.is_cuda
     dev = _dev_of(ys_bar, as_, out)
@@ -213,7 +214,7 @@ def scan(op, ys_bar: torch.Tensor, as_: torch.Tensor | None = None, *, out: torc
     _check(L.vjp_scan(o, _dt(yb), n, _p(a), _p(yb), _p(ab), _p(ys), _p(ws),
                       0 if ws is None else ws.numel(), _stream(dev),
                       (ACCUMULATE if accumulate else 0) | (SCAN_LOOKBACK if lookback else 0)
-                      | (SCAN_SWEEP if sweep else 0)),
+                      | (SCAN_SWEEP if sweep else 0) | (SCAN_CHUNKED if chunked else 0)),
            "vjp_scan")
     if out is not None and not out.is_cuda:
         out.copy_(ab, non_blocking=True)

@@ -284,8 +284,14 @@ struct ScanImpl {
     static constexpr int SW_S_1 = 4;  // TMA stages when a stage is one 16 KB buffer
     static constexpr int SW_S_2 = 3;  // ... two or three buffers
 
+    // the one-read sweep is the default for scan(+) without ys on one GPU (its
+    // reverse maps commute: 3.74 vs 4.10 ms at 2^30 f64); the other operators
+    // take it only on request (their shuffle scans of d-vector maps make it
+    // slower than the chunked kernels)
     static bool use_sweep(const ScanCall &c) {
-        return c.world == 1 && (c.flags & VJP_SCAN_SWEEP) && !(c.flags & VJP_SCAN_LOOKBACK);
+        if (c.world != 1 || (c.flags & (VJP_SCAN_LOOKBACK | VJP_SCAN_CHUNKED))) return false;
+        if (c.flags & VJP_SCAN_SWEEP) return true;
+        return std::is_same<Op, vjpk::OpAdd>::value && c.ys == nullptr && env_int("VJP_SCAN_NO_SWEEP", 0) == 0;
     }
 
     template <bool FWD, bool ACC, bool YS>
@@ -343,6 +349,7 @@ struct ScanImpl {
         // tiles per CTA per round: about `round_mb` MB of HBM-read input per round
         const int64_t round_bytes = (int64_t)env_int("VJP_SWEEP_ROUND_MB", 32) << 20;
         int64_t K = round_bytes / (G * NBR * NTC * vjpk::kRowBytes);
+        if (std::is_same<Op, vjpk::OpAdd>::value) K = 4;  // measured best for scan(+) at 2^26..2^30 (DESIGN 7.6)
         K = env_int("VJP_SWEEP_K", (int)K);
         if (K < 1) K = 1;
         if (K > vjpk::kSweepKMax) K = vjpk::kSweepKMax;

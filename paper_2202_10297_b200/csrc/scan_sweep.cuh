@@ -37,6 +37,8 @@
 // pre-pass K_F = scan_reduce<FWD only> and scan_tile_prefix.
 #pragma once
 
+#include <type_traits>
+
 #include "scan_chunked.cuh"
 
 namespace vjpk {
@@ -376,6 +378,10 @@ __global__ void __launch_bounds__(NT + 64, (FWD || ACC) ? 2 : 3) scan_sweep(cons
     const uint64_t pol = HINT ? make_policy_evict_first() : 0ull;
     V X;              // reverse carry entering the current tile from the right (every warp)
     int64_t job = 0;
+    // ADD: the reverse maps X -> D + X commute, so a reduce segment needs no
+    // per-tile ordering: every thread sums its rows over the segment's tiles
+    constexpr bool kComm = std::is_same<Op, OpAdd>::value;
+    M mthr = Op::map_id();
     int pend = -1;    // stage whose empty-arrive waits for this warp's TMA store to read it
 
     for (int s = 0; s < sweep_nseg(sp); ++s) {
@@ -410,11 +416,28 @@ __global__ void __launch_bounds__(NT + 64, (FWD || ACC) ? 2 : 3) scan_sweep(cons
                     }
                     mbar_arrive(&ss.empty[st]);
                 }
-                m = warp_suffix_maps<Op>(m, lane);
-                if (lane == 0 && i < kSweepKMax) ss.ragg[rslot][i][warp] = m;
+                if constexpr (kComm) {
+                    mthr = Op::compose(m, mthr);  // commutative maps: per-thread sum over the tiles
+                } else {
+                    m = warp_suffix_maps<Op>(m, lane);
+                    if (lane == 0 && i < kSweepKMax) ss.ragg[rslot][i][warp] = m;
+                }
+            }
+            if constexpr (kComm) {  // one warp reduction per segment instead of one per tile
+                mthr = warp_suffix_maps<Op>(mthr, lane);
+                if (lane == 0) ss.ragg[rslot][0][warp] = mthr;
+                mthr = Op::map_id();
             }
             bar_tiles();
-            if (warp == 1) {
+            if (kComm && warp == 1) {
+                if (lane == 0) {
+                    M seg = Op::map_id();
+#pragma unroll
+                    for (int w2 = 0; w2 < NWT; ++w2) seg = Op::compose(ss.ragg[rslot][0][w2], seg);
+                    ss.rec[slot] = seg;
+                    mbar_arrive(&ss.recbar[slot]);
+                }
+            } else if (warp == 1) {
                 // E_k, k = 4i + (3 - w): tiles right to left, warps right to left within a tile
                 M seg = Op::map_id();
                 for (int b = 0; b < cnt * NWT; b += 32) {

@@ -111,7 +111,7 @@ def test_scan_add_integer_seeds_bit_exact(dt):
     for n in (10_000, 1 << 20, (1 << 20) + 3, 5_000_011):
         yb = synth.scan_add_seed(n, kind="int", dtype=TD[dt])
         ref = oracle.vjp_scan("add", yb.numpy(), None)
-        for kw in ({}, {"lookback": True}, {"sweep": True}):
+        for kw in ({}, {"lookback": True}, {"sweep": True}, {"chunked": True}):
             got = vjp.scan("add", yb.to(DEV), **kw).cpu().numpy()
             assert np.array_equal(got, ref), kw
 
@@ -195,9 +195,9 @@ def test_scan_add_2pow30_sampled():
     got = vjp.scan("add", yb)
     exact = torch.flip(torch.cumsum(torch.flip(yb.to(torch.int64), [0]), 0), [0])
     assert torch.equal(got.to(torch.int64), exact)
-    got_sw = vjp.scan("add", yb, sweep=True)  # many rounds of the L2-round sweep
-    assert torch.equal(got_sw.to(torch.int64), exact)
-    del got_sw
+    got_ch = vjp.scan("add", yb, chunked=True)  # (the default above is the L2-round sweep)
+    assert torch.equal(got_ch.to(torch.int64), exact)
+    del got_ch
     # sampled comparison against the oracle on a slice near the end (independent of the prefix)
     tail = yb[-100_000:].cpu().numpy()
     ref_tail = oracle.vjp_scan("add", tail, None)
