@@ -375,6 +375,13 @@ struct ScanImpl {
                     (long long)L.ntiles_c);
         void *args[] = {&ma, &my, &mab, &mab32, &mys32, &sp};
         cudaError_t e = cudaLaunchCooperativeKernel((const void *)k, dim3((unsigned)G), dim3(NTH), args, sm, c.stream);
+        if (e == cudaErrorCooperativeLaunchTooLarge) {
+            // the GPU cannot hold all CTAs at once right now (e.g. another kernel is
+            // resident): the sweep's round synchronisation would not be safe, so
+            // the call takes the chunked kernels instead (same results)
+            (void)cudaGetLastError();
+            return VJP_EUNSUPPORTED;
+        }
         count_launch();
         return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
     }
@@ -390,11 +397,18 @@ struct ScanImpl {
             count_launch();
             if (cudaGetLastError() != cudaSuccess) return VJP_ECUDA;
         }
-        if constexpr (std::is_same<Op, vjpk::OpAdd>::value) {
-            if (!ys) return acc ? launch_sweep<false, true, false>(c, L) : launch_sweep<false, false, false>(c, L);
+        vjp_status st;
+        if (std::is_same<Op, vjpk::OpAdd>::value && !ys)
+            st = acc ? launch_sweep<false, true, false>(c, L) : launch_sweep<false, false, false>(c, L);
+        else if (acc)
+            st = ys ? launch_sweep<true, true, true>(c, L) : launch_sweep<true, true, false>(c, L);
+        else
+            st = ys ? launch_sweep<true, false, true>(c, L) : launch_sweep<true, false, false>(c, L);
+        if (st == VJP_EUNSUPPORTED) {  // cooperative launch refused: the chunked kernels
+            vjp_status s2 = partial_c(c);
+            return s2 == VJP_OK ? finish_c(c) : s2;
         }
-        if (acc) return ys ? launch_sweep<true, true, true>(c, L) : launch_sweep<true, true, false>(c, L);
-        return ys ? launch_sweep<true, false, true>(c, L) : launch_sweep<true, false, false>(c, L);
+        return st;
     }
 
     // ---------------- general reduce rule, LINREC / MAT2 ----------------
