@@ -33,6 +33,7 @@ constexpr int kBThreads = 256;
 #define VJP_RBI_MINB 4
 #endif
 constexpr int kBMinBlocks = VJP_RBI_MINB;
+constexpr int64_t kSmallM = 16384;  // per-bin tables that stay in L1 / shared memory
 
 template <class I>
 struct IdxVec;
@@ -452,7 +453,7 @@ __global__ void rbi_mul_prep(const T *__restrict__ hs_bar, const double *__restr
 // ADD (gather) and MUL (three cases) return map; lane-contiguous 4-element
 // groups, two slabs per iteration for 8 independent gathers in flight per lane
 template <class T, class I, int OP>
-__global__ void __launch_bounds__(kBThreads) rbi_bwd_map(const I *__restrict__ inds, const T *__restrict__ as,
+__device__ __forceinline__ void rbi_bwd_map_body(const I *__restrict__ inds, const T *__restrict__ as,
                                                          const T *__restrict__ hs_bar, const MulPack<T> *__restrict__ pk,
                                                          T *__restrict__ ab, int64_t n, int64_t m, int acc, int v256) {
     const uint64_t pol = policy_evict_first();
@@ -515,6 +516,19 @@ __global__ void __launch_bounds__(kBThreads) rbi_bwd_map(const I *__restrict__ i
             }
         }
     }
+}
+template <class T, class I, int OP>
+__global__ void __launch_bounds__(kBThreads) rbi_bwd_map(const I *__restrict__ inds, const T *__restrict__ as,
+                                                         const T *__restrict__ hs_bar, const MulPack<T> *__restrict__ pk,
+                                                         T *__restrict__ ab, int64_t n, int64_t m, int acc, int v256) {
+    rbi_bwd_map_body<T, I, OP>(inds, as, hs_bar, pk, ab, n, m, acc, v256);
+}
+// small per-bin tables (L1 hits): capped at 64 registers -> 4 CTAs/SM (MUL m = 1e3)
+template <class T, class I, int OP>
+__global__ void __launch_bounds__(kBThreads, kBMinBlocks) rbi_bwd_map_small(const I *__restrict__ inds, const T *__restrict__ as,
+                                                         const T *__restrict__ hs_bar, const MulPack<T> *__restrict__ pk,
+                                                         T *__restrict__ ab, int64_t n, int64_t m, int acc, int v256) {
+    rbi_bwd_map_body<T, I, OP>(inds, as, hs_bar, pk, ab, n, m, acc, v256);
 }
 
 // MIN/MAX return: scatter hs_bar[b] to the winner of every bin (as_bar was
@@ -735,7 +749,10 @@ vjp_status run_full(vjp_op op, int64_t n, int64_t m, const void *inds_, const vo
     if (op == VJP_MUL) {
         MulPack<T> *pk = reinterpret_cast<MulPack<T> *>(static_cast<unsigned char *>(ws) + L.pk);
         rbi_mul_prep<T><<<grid_for(m, 4), kBThreads, 0, s>>>(hsb, P.p, P.z, pk, m, hs, winners);
-        rbi_bwd_map<T, I, VJP_MUL><<<grid_resident(rbi_bwd_map<T, I, VJP_MUL>, n / 4 + 1), kBThreads, 0, s>>>(inds, as, hsb, pk, ab, n, m, acc, (int)(a32(as) && a32(ab)));
+        if (m <= kSmallM)  // small table (L1 hits): 4 CTAs/SM hide the stream latency
+            rbi_bwd_map_small<T, I, VJP_MUL><<<grid_resident(rbi_bwd_map_small<T, I, VJP_MUL>, n / 4 + 1), kBThreads, 0, s>>>(inds, as, hsb, pk, ab, n, m, acc, (int)(a32(as) && a32(ab)));
+        else
+            rbi_bwd_map<T, I, VJP_MUL><<<grid_resident(rbi_bwd_map<T, I, VJP_MUL>, n / 4 + 1), kBThreads, 0, s>>>(inds, as, hsb, pk, ab, n, m, acc, (int)(a32(as) && a32(ab)));
         vjph::count_launch(2);
     } else if (op == VJP_MIN) {
         rbi_ext_scatter<T, VJP_MIN><<<grid_for(m, 4), kBThreads, 0, s>>>(P.win, hsb, ab, m, 0, n, acc, hs, winners);
@@ -783,7 +800,10 @@ vjp_status run_finish(vjp_op op, int64_t n, int64_t m, int64_t goff, const void 
         MulPack<T> *pk = reinterpret_cast<MulPack<T> *>(static_cast<unsigned char *>(ws) + L.pk);
         rbi_mul_prep_ext<T><<<grid_for(m, 4), kBThreads, 0, s>>>(hsb, bin_val, bin_aux, pk, m);
         vjph::count_launch();
-        rbi_bwd_map<T, I, VJP_MUL><<<grid_resident(rbi_bwd_map<T, I, VJP_MUL>, n / 4 + 1), kBThreads, 0, s>>>(inds, as, hsb, pk, ab, n, m, acc, (int)(a32(as) && a32(ab)));
+        if (m <= kSmallM)  // small table (L1 hits): 4 CTAs/SM hide the stream latency
+            rbi_bwd_map_small<T, I, VJP_MUL><<<grid_resident(rbi_bwd_map_small<T, I, VJP_MUL>, n / 4 + 1), kBThreads, 0, s>>>(inds, as, hsb, pk, ab, n, m, acc, (int)(a32(as) && a32(ab)));
+        else
+            rbi_bwd_map<T, I, VJP_MUL><<<grid_resident(rbi_bwd_map<T, I, VJP_MUL>, n / 4 + 1), kBThreads, 0, s>>>(inds, as, hsb, pk, ab, n, m, acc, (int)(a32(as) && a32(ab)));
     } else {
         rbi_ext_gather<T, I><<<grid_for(n, 8), kBThreads, 0, s>>>(inds, hsb, bin_aux, ab, n, m, goff, acc);
     }
