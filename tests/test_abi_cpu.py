@@ -133,3 +133,32 @@ def test_carries_host_add(L):
                                        fwd.ctypes.data_as(ctypes.c_void_p),
                                        rev.ctypes.data_as(ctypes.c_void_p)) == 0
         assert rev[0] == pytest.approx(sums[r + 1:].sum(), rel=1e-15)
+
+
+def test_extension_entry_points_validate_without_gpu(L):
+    """vjp_scan_batched / vjp_kmeans / vjp_scan_partial2 / the general reduce
+    reject bad arguments before any launch (no GPU needed)."""
+    vp = ctypes.c_void_p
+    buf = (ctypes.c_double * 64)()
+    p = ctypes.addressof(buf)
+    p16 = vp(p + (16 - p % 16) % 16)
+    # workspace queries
+    assert L.vjp_scan_batched_workspace_bytes(1, 2, 1000, 8) > 0
+    assert L.vjp_scan_batched_workspace_bytes(3, 2, 1000, 8) > 0       # MIN batched is offered
+    assert L.vjp_scan_batched_workspace_bytes(1, 2, 1000, 0) == 0      # width < 1
+    assert L.vjp_kmeans_workspace_bytes(2, 1000, 16, 8) > 0
+    assert L.vjp_kmeans_workspace_bytes(2, 1000, 0, 8) == 0
+    assert L.vjp_reduce_workspace_bytes(6, 2, 1000) > 0                # MAT2: the general rule's workspace
+    # argument errors
+    assert L.vjp_scan_batched(1, 2, 10, 0, None, p16, p16, p16, 1 << 20, None, 0) == 1   # width 0 -> EINVAL
+    assert L.vjp_scan_batched(9, 2, 10, 2, None, p16, p16, p16, 1 << 20, None, 0) == 1   # bad tag
+    assert L.vjp_scan_batched(5, 2, 10, 2, None, p16, vp(p16.value + 256), p16, 1 << 20, None, 0) == 1  # LINREC needs as
+    assert L.vjp_kmeans(2, 10, 0, 4, p16, p16, p16, p16, None, None, None, None, p16, 1 << 20, None, 0) == 1
+    assert L.vjp_kmeans(2, 10, 20_000, 4, p16, p16, p16, p16, None, None, None, None, p16, 1 << 20, None, 0) == 2
+    assert L.vjp_kmeans(2, 10, 4, 4, p16, p16, p16, p16, None, None, None, None, p16, 0, None, 0) == 3  # workspace
+    from paper_2202_10297_b200 import VjpShard
+    sh = VjpShard(0, 2, 0, 20)
+    assert L.vjp_scan_partial2(1, 2, 10, None, p16, p16, 1 << 20, sh, p16, p16, None, 0) == 2  # ADD: one exchange
+    sh1 = VjpShard(0, 1, 0, 10)
+    assert L.vjp_scan_partial2(3, 2, 10, p16, p16, p16, 1 << 20, sh1, p16, p16, None, 0) == 1  # world 1
+    assert L.vjp_reduce(6, 2, 10, None, p16, p16, None, None, p16, 1 << 20, None, 0) == 1    # MAT2 needs as
