@@ -200,8 +200,10 @@ vjp_status vjp_scan_carries_host(vjp_op op, vjp_dtype dtype, int32_t rank, int32
     case VJP_MUL: carries_host<vjpk::OpMul>(g, rank, world, fwd_carry, rev_carry); return VJP_OK;
     case VJP_LINREC: carries_host<vjpk::OpLinrec>(g, rank, world, fwd_carry, rev_carry); return VJP_OK;
     case VJP_MAT2: carries_host<vjpk::OpMat2>(g, rank, world, fwd_carry, rev_carry); return VJP_OK;
-    case VJP_MIN:
-    case VJP_MAX: return VJP_EUNSUPPORTED;
+    // MIN/MAX (two exchanges): call with the first gathered array for the
+    // forward carry and with the second one for the reverse carry
+    case VJP_MIN: carries_host<vjpk::OpMin>(g, rank, world, fwd_carry, rev_carry); return VJP_OK;
+    case VJP_MAX: carries_host<vjpk::OpMax>(g, rank, world, fwd_carry, rev_carry); return VJP_OK;
     }
     return VJP_EINVAL;
 }

@@ -1,7 +1,8 @@
 """Multi-process (world_size 2, gloo, CPU) checks of the host-side logic of
 the multi-GPU path: contiguous shard bounds, the rank-ordered all_gather of
 per-shard scan records feeding the carry combination (vjp_scan_carries_host,
-the same __host__ __device__ code the finish kernel runs), and the
+the same __host__ __device__ code the finish kernel runs), the two-exchange
+protocol of the MIN/MAX scans, and the
 reduce_by_index max/min winner protocol (all_reduce MAX of values, candidate
 selection, all_reduce MIN of global indices) — each against the oracle on the
 unsharded array."""
@@ -73,6 +74,51 @@ def _worker(rank, world, port, q):
         for j in range(N - 1, off + n - 1, -1):
             H = (Y[j] + H) @ A[j].T
         np.testing.assert_allclose(rev, H.ravel(), rtol=1e-12, atol=1e-300)
+
+        # ---- scan MIN across ranks: the two-exchange protocol -------------
+        # exchange 1: forward aggregates; exchange 2: the reverse-map aggregates
+        # built with the forward carry (pick-left Jacobians need rs); then each
+        # rank's return sweep from the combined carries equals the oracle slice
+        N = 41
+        a = (synth.integers(N, 9, 0, 5).to(torch.float64) / 4.0).numpy()
+        yv = synth.uniform(N, 10).numpy()
+        off, n = shard_bounds(N, world, rank)
+        F = float("inf")
+        for v in a[off:off + n]:
+            F = F if F <= v else v
+        r1 = torch.tensor([F, 0.0, 1.0], dtype=torch.float64)
+        b1 = [torch.empty_like(r1) for _ in range(world)]
+        dist.all_gather(b1, r1)
+        g1 = torch.cat(b1).contiguous().numpy()
+        fwd, rev = np.zeros(1), np.zeros(1)
+        assert L.vjp_scan_carries_host(3, 2, rank, world, g1.ctypes.data_as(ctypes.c_void_p),
+                                       fwd.ctypes.data_as(ctypes.c_void_p), rev.ctypes.data_as(ctypes.c_void_p)) == 0
+        exp_f = float("inf")
+        for v in a[:off]:
+            exp_f = exp_f if exp_f <= v else v
+        assert fwd[0] == exp_f
+        rs = fwd[0]  # maps with the true rs: M_i(X) = [rs_{i-1} <= a_i] (ybar_i + X), composed right to left
+        Dm, Cm = 0.0, 1.0
+        jl = []
+        for v in a[off:off + n]:
+            jl.append(1.0 if rs <= v else 0.0)
+            rs = rs if rs <= v else v
+        for i in range(n - 1, -1, -1):  # M = M_lo o ... o M_hi
+            Dm, Cm = jl[i] * (yv[off + i] + Dm), jl[i] * Cm
+        r2 = torch.tensor([float("inf"), Dm, Cm], dtype=torch.float64)
+        b2 = [torch.empty_like(r2) for _ in range(world)]
+        dist.all_gather(b2, r2)
+        g2 = torch.cat(b2).contiguous().numpy()
+        assert L.vjp_scan_carries_host(3, 2, rank, world, g2.ctypes.data_as(ctypes.c_void_p),
+                                       fwd.ctypes.data_as(ctypes.c_void_p), rev.ctypes.data_as(ctypes.c_void_p)) == 0
+        H = rev[0]
+        out = np.zeros(n)
+        for i in range(n - 1, -1, -1):
+            g = yv[off + i] + H
+            out[i] = g if off + i == 0 else (1.0 - jl[i]) * g
+            H = jl[i] * g
+        ref = oracle.vjp_scan("min", yv, a)
+        np.testing.assert_allclose(out, ref[off:off + n], rtol=1e-14, atol=0)
 
         # ---- reduce_by_index MAX winners: the 3-step collective protocol ----
         M, NN = 50, 2000
