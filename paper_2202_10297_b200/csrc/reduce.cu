@@ -255,7 +255,26 @@ __global__ void __launch_bounds__(kRThreads) reduce_bwd(const T *__restrict__ as
     if (!p.acc) {
         // overwrite mode: 4 independent 16-byte vectors per thread per iteration
         int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-        if (need_a) {  // MUL, no zero: as_bar_i = ybar * p / a_i
+        // f32 data: the quotient is rounded to f32 anyway, so divide in f32 when
+        // q = ybar * p is a normal f32 (one extra f32 rounding: <= 1.5 ulp f32,
+        // far inside 1e-4); the f64 division made this loop compute bound
+        const bool f32div = sizeof(T) == 4 && fabs(q) < 1e37 && fabs(q) > 1e-37;
+        if (need_a && f32div) {
+            const float qf = (float)q;
+            for (; j + 3 * stride < nv; j += 4 * stride) {
+                typename VV::V v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = __ldcs(av + j + u * stride);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    double a[VV::N], r[VV::N];
+                    VV::get(v[u], a);
+#pragma unroll
+                    for (int q2 = 0; q2 < VV::N; ++q2) r[q2] = (double)(qf / (float)a[q2]);
+                    __stcs(bv + j + u * stride, VV::make(r));
+                }
+            }
+        } else if (need_a) {  // MUL, no zero: as_bar_i = ybar * p / a_i
             for (; j + 3 * stride < nv; j += 4 * stride) {
                 typename VV::V v[4];
 #pragma unroll
