@@ -66,6 +66,12 @@ __device__ __forceinline__ void km_stage(double *dst, const double *src, bool ok
                  : "memory");
 }
 __device__ __forceinline__ void km_stage(double *dst, const float *src, bool ok) { *dst = ok ? (double)*src : 0.0; }
+// two f64 elements by one 16-byte cp.async.cg (even d, 16-byte aligned rows)
+__device__ __forceinline__ void km_stage16(double *dst, const double *src, bool ok) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(ok ? src : nullptr), "r"(ok ? 16 : 0)
+                 : "memory");
+}
 __device__ __forceinline__ void km_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void km_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -249,7 +255,7 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
 
 constexpr int KM_MMA_NT = 256;  // 8 warps: 4 point groups x 2 center halves
 
-template <class T, bool RES>
+template <class T, bool RES, bool V16 = false>
 __global__ void __launch_bounds__(KM_MMA_NT, 2) km_assign_mma(const T *__restrict__ P, const T *__restrict__ C,
                                                               const double *__restrict__ cn, int64_t n, int64_t k,
                                                               int64_t d, int32_t *__restrict__ assign,
@@ -269,12 +275,22 @@ __global__ void __launch_bounds__(KM_MMA_NT, 2) km_assign_mma(const T *__restric
         const int ct = st / nd, dc = st % nd, buf = st & 1;
         const int64_t c0 = (int64_t)ct * KM_BC, d0 = (int64_t)dc * KM_KD;
         double *cs = Cs + (size_t)buf * KM_BC * CW;
+        if constexpr (V16) {
 #pragma unroll 2
-        for (int idx = t; idx < KM_BC * KM_KD; idx += KM_MMA_NT) {
-            const int cc = idx / KM_KD, kk = idx % KM_KD;
-            const int64_t gc = c0 + cc, gd = d0 + kk;
-            const bool ok = gc < k && gd < d;
-            km_stage(cs + cc * CW + kk, C + (ok ? gc * d + gd : 0), ok);
+            for (int idx = t; idx < KM_BC * KM_KD / 2; idx += KM_MMA_NT) {
+                const int cc = idx / (KM_KD / 2), kk = 2 * (idx % (KM_KD / 2));
+                const int64_t gc = c0 + cc, gd = d0 + kk;
+                const bool ok = gc < k && gd < d;
+                km_stage16(cs + cc * CW + kk, reinterpret_cast<const double *>(C) + (ok ? gc * d + gd : 0), ok);
+            }
+        } else {
+#pragma unroll 2
+            for (int idx = t; idx < KM_BC * KM_KD; idx += KM_MMA_NT) {
+                const int cc = idx / KM_KD, kk = idx % KM_KD;
+                const int64_t gc = c0 + cc, gd = d0 + kk;
+                const bool ok = gc < k && gd < d;
+                km_stage(cs + cc * CW + kk, C + (ok ? gc * d + gd : 0), ok);
+            }
         }
         if (!RES) {
             double *ps = Ps + (size_t)buf * KM_BP * PW;
@@ -290,12 +306,22 @@ __global__ void __launch_bounds__(KM_MMA_NT, 2) km_assign_mma(const T *__restric
     };
     if (RES) {
         const int DP = nd * KM_KD;
+        if constexpr (V16) {
 #pragma unroll 4
-        for (int idx = t; idx < KM_BP * DP; idx += KM_MMA_NT) {
-            const int pp = idx / DP, kk = idx % DP;
-            const int64_t gp = p0 + pp;
-            const bool ok = gp < n && kk < d;
-            km_stage(Ps + pp * PW + kk, P + (ok ? gp * d + kk : 0), ok);
+            for (int idx = t; idx < KM_BP * DP / 2; idx += KM_MMA_NT) {
+                const int pp = idx / (DP / 2), kk = 2 * (idx % (DP / 2));
+                const int64_t gp = p0 + pp;
+                const bool ok = gp < n && kk < d;
+                km_stage16(Ps + pp * PW + kk, reinterpret_cast<const double *>(P) + (ok ? gp * d + kk : 0), ok);
+            }
+        } else {
+#pragma unroll 4
+            for (int idx = t; idx < KM_BP * DP; idx += KM_MMA_NT) {
+                const int pp = idx / DP, kk = idx % DP;
+                const int64_t gp = p0 + pp;
+                const bool ok = gp < n && kk < d;
+                km_stage(Ps + pp * PW + kk, P + (ok ? gp * d + kk : 0), ok);
+            }
         }
     }
     stage(0);
@@ -673,7 +699,11 @@ vjp_status km_run(int64_t n, int64_t k, int64_t d, const void *P, const void *C,
             const int PW = (res ? (int)nd * vjpk::KM_KD : vjpk::KM_KD) + vjpk::KM_PS_PAD;
             const size_t msm = ((size_t)(res ? 1 : 2) * vjpk::KM_BP * PW +
                                 (size_t)2 * vjpk::KM_BC * (vjpk::KM_KD + vjpk::KM_PS_PAD)) * 8;
-            auto km = res ? vjpk::km_assign_mma<T, true> : vjpk::km_assign_mma<T, false>;
+            // 16-byte staging copies for f64 with even d (rows 16-byte aligned)
+            const bool v16 = sizeof(T) == 8 && (d % 2) == 0 && (reinterpret_cast<uintptr_t>(Pt) % 16) == 0 &&
+                             (reinterpret_cast<uintptr_t>(Ct) % 16) == 0;
+            auto km = res ? (v16 ? vjpk::km_assign_mma<T, true, true> : vjpk::km_assign_mma<T, true, false>)
+                          : (v16 ? vjpk::km_assign_mma<T, false, true> : vjpk::km_assign_mma<T, false, false>);
             cudaFuncSetAttribute(km, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msm);
             km<<<(unsigned)L.nbA, vjpk::KM_MMA_NT, msm, s>>>(Pt, Ct, cn, n, k, d, asg, part);
         } else {
