@@ -9,6 +9,7 @@
  *   vjp_reduce           sec 5.1, P:971-1087    (reduce; special cases + * min max)
  *   vjp_reduce_by_index  sec 5.1.2, P:1090-1126 (histogram / multi-reduce)
  *   vjp_scatter          sec 5.3
+ *   vjp_scatter_forward / vjp_scatter_restore   sec 5.3
  *
  * "P:n" is line n of PAPER.md.  Every entry point takes the primal inputs, an
  * operator tag and the output adjoint, and writes the input adjoint(s) by the
@@ -289,7 +290,8 @@ vjp_status vjp_reduce_by_index_finish(vjp_op op, vjp_dtype dtype, vjp_itype ityp
  * skipped and their vs_bar is 0 (reading R4).  xs_bar MAY alias ys_bar: then
  * the call is in place and its work is O(m), independent of n;
  * otherwise ys_bar is first copied to xs_bar (O(n)).  The paper's step (3),
- * restoring the primal xs, is not part of the adjoint and is not done here.
+ * restoring the primal xs, is not part of the adjoint: vjp_scatter_restore
+ * (below) does it.
  *   is [m] int32/int64; ys_bar [n x width]; xs_bar [n x width]; vs_bar [m x width].
  * VJP_CHECK_INDICES: validates `is` first (synchronises the stream) and
  * returns VJP_EDUPINDEX / VJP_EOOB without touching the outputs; it needs a
@@ -301,6 +303,33 @@ size_t vjp_scatter_workspace_bytes(vjp_dtype dtype, int64_t n, int64_t m);
 vjp_status vjp_scatter(vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, int64_t width,
                        const void *is, const void *ys_bar, void *xs_bar, void *vs_bar, void *ws,
                        size_t ws_bytes, vjp_stream_t stream, unsigned flags);
+
+/* ======================================================================
+ * vjp_scatter_forward / vjp_scatter_restore — the in-place scatter's forward
+ * save and the return sweep's step (3) (sec 5.3)
+ *
+ * The in-place update `let xs = scatter xs is vs` overwrites xs, so the
+ * forward sweep first saves the elements about to be overwritten:
+ *     xs_saved = gather xs is;  xs = scatter xs is vs
+ * and the return sweep, after vjp_scatter, restores the primal:
+ *     xs = scatter ys is xs_saved
+ * vjp_scatter_forward: xs [n x width] is updated IN PLACE (it becomes ys);
+ *   xs_saved [m x width] is written (out-of-range targets: skipped, saved 0,
+ *   reading R4); vs [m x width] is read.
+ * vjp_scatter_restore: ys [n x width] is updated IN PLACE (it becomes xs
+ *   again) from xs_saved; out-of-range targets are skipped.
+ * Both are O(m): one thread per (target, component), nothing proportional to
+ * n is touched.  DEVICE pointers, 16-byte aligned; `is` must hold no
+ * duplicate in-range target — with VJP_CHECK_INDICES (forward
+ * only; needs vjp_scatter_workspace_bytes of ws, synchronises) a violation
+ * returns VJP_EDUPINDEX / VJP_EOOB before anything is written.  flags other
+ * than VJP_CHECK_INDICES are rejected (VJP_EINVAL).
+ * ==================================================================== */
+vjp_status vjp_scatter_forward(vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, int64_t width,
+                               const void *is, const void *vs, void *xs, void *xs_saved, void *ws,
+                               size_t ws_bytes, vjp_stream_t stream, unsigned flags);
+vjp_status vjp_scatter_restore(vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, int64_t width,
+                               const void *is, const void *xs_saved, void *ys, vjp_stream_t stream);
 
 /* Test hook: y[i] = log2|x[i]| (DEVICE arrays, f64) by the routine the MUL
  * histograms accumulate with (reduce_by_index log domain). */

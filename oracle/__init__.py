@@ -171,6 +171,42 @@ def vjp_scatter(is_: np.ndarray, ys_bar: np.ndarray, *, width: int = 1, vs_out=N
     return xs_bar, vs_bar, rc
 
 
+def gather(arr: np.ndarray, inds: np.ndarray, *, width: int = 1) -> np.ndarray:
+    """``gather arr inds = map (\\i -> arr[i]) inds``, elements of
+    `width` scalars; an out-of-range index reads 0 (reading R4)."""
+    a = np.asarray(arr).reshape(-1, width)
+    out = np.zeros((len(inds), width), dtype=a.dtype)
+    for j, t in enumerate(np.asarray(inds).tolist()):
+        if 0 <= t < a.shape[0]:
+            out[j] = a[t]
+    return out.reshape(-1)
+
+
+def scatter(arr: np.ndarray, inds: np.ndarray, vals: np.ndarray, *, width: int = 1) -> np.ndarray:
+    """``scatter arr inds vals``: a copy of arr with arr[inds[j]] = vals[j]
+    (P:1241-1244); out-of-range indices are skipped (reading R4)."""
+    a = np.array(arr, copy=True).reshape(-1, width)
+    v = np.asarray(vals).reshape(-1, width)
+    for j, t in enumerate(np.asarray(inds).tolist()):
+        if 0 <= t < a.shape[0]:
+            a[t] = v[j]
+    return a.reshape(-1)
+
+
+def scatter_forward(xs: np.ndarray, is_: np.ndarray, vs: np.ndarray, *, width: int = 1):
+    """Forward sweep of the in-place scatter, in the paper's order:
+    ``let xs_saved = gather xs is; let ys = scatter xs is vs``.
+    Returns (ys, xs_saved).  Pure-Python loop over m: small cases only."""
+    xs_saved = gather(xs, is_, width=width)
+    ys = scatter(xs, is_, vs, width=width)
+    return ys, xs_saved
+
+
+def scatter_restore(ys: np.ndarray, is_: np.ndarray, xs_saved: np.ndarray, *, width: int = 1) -> np.ndarray:
+    """Return sweep step (3): ``let xs = scatter ys is xs_saved``."""
+    return scatter(ys, is_, xs_saved, width=width)
+
+
 def kmeans(points: np.ndarray, centers: np.ndarray, cost_bar: float = 1.0):
     """k-means cost f(C) = sum_p min_j ||p - c_j||^2 and its derivatives by the
     literal per-point loop (oracle.c; reading R15).

@@ -80,6 +80,8 @@ def lib():
             "vjp_reduce_by_index_finish": ([ci, ci, ci, i64, i64, vp, vp, vp, vp, vp, vp, vp, sz, sp, vp, u32], ci),
             "vjp_scatter_workspace_bytes": ([ci, i64, i64], sz),
             "vjp_scatter": ([ci, ci, i64, i64, i64, vp, vp, vp, vp, vp, sz, vp, u32], ci),
+            "vjp_scatter_forward": ([ci, ci, i64, i64, i64, vp, vp, vp, vp, vp, sz, vp, u32], ci),
+            "vjp_scatter_restore": ([ci, ci, i64, i64, i64, vp, vp, vp, vp], ci),
             "vjp_kmeans_workspace_bytes": ([ci, i64, i64, i64], sz),
             "vjp_scan_batched_workspace_bytes": ([ci, ci, i64, i64], sz),
             "vjp_debug_log2_abs": ([vp, vp, i64, vp], ci),
@@ -321,6 +323,42 @@ def scatter(is_: torch.Tensor, ys_bar: torch.Tensor, *, width: int = 1, in_place
     _check(L.vjp_scatter(_dt(yb), _it(ix), n, m, width, _p(ix), _p(yb), _p(xb), _p(vb), _p(ws),
                          0 if ws is None else ws.numel(), _stream(dev), flags), "vjp_scatter")
     return _host_out(xb, host), _host_out(vb, host)
+
+
+def scatter_forward(xs: torch.Tensor, is_: torch.Tensor, vs: torch.Tensor, *, width: int = 1,
+                    saved_out: torch.Tensor | None = None, check: bool = False) -> torch.Tensor:
+    """Forward sweep of the in-place ``let xs = scatter xs is vs``:
+    returns xs_saved = gather xs is and updates the DEVICE tensor xs in place
+    (it becomes ys).  O(m)."""
+    if not xs.is_cuda:
+        raise ValueError("scatter_forward updates xs in place: it must be a device tensor")
+    dev = xs.device
+    ix, v = _to(is_, dev), _to(vs, dev)
+    n, m = xs.numel() // width, ix.numel()
+    if v.numel() != m * width or v.dtype != xs.dtype:
+        raise ValueError("vs must be [m x width] of xs's dtype")
+    saved = saved_out if saved_out is not None else torch.empty(m * width, dtype=xs.dtype, device=dev)
+    L = lib()
+    ws = workspace(L.vjp_scatter_workspace_bytes(_dt(xs), n, m), dev) if check else None
+    _check(L.vjp_scatter_forward(_dt(xs), _it(ix), n, m, width, _p(ix), _p(v), _p(xs), _p(saved), _p(ws),
+                                 0 if ws is None else ws.numel(), _stream(dev), CHECK_INDICES if check else 0),
+           "vjp_scatter_forward")
+    return saved
+
+
+def scatter_restore(ys: torch.Tensor, is_: torch.Tensor, xs_saved: torch.Tensor, *, width: int = 1) -> torch.Tensor:
+    """Return sweep step (3): ``xs = scatter ys is xs_saved`` on the
+    DEVICE tensor ys, in place; returns it.  O(m)."""
+    if not ys.is_cuda:
+        raise ValueError("scatter_restore updates ys in place: it must be a device tensor")
+    dev = ys.device
+    ix, sv = _to(is_, dev), _to(xs_saved, dev)
+    n, m = ys.numel() // width, ix.numel()
+    if sv.numel() != m * width or sv.dtype != ys.dtype:
+        raise ValueError("xs_saved must be [m x width] of ys's dtype")
+    _check(lib().vjp_scatter_restore(_dt(ys), _it(ix), n, m, width, _p(ix), _p(sv), _p(ys), _stream(dev)),
+           "vjp_scatter_restore")
+    return ys
 
 
 def kmeans(points: torch.Tensor, centers: torch.Tensor, cost_bar=1.0, *, hess: bool = True,

@@ -7,7 +7,9 @@
 // same thread, so the in-place form (xs_bar aliasing ys_bar) is race free given
 // distinct targets (the precondition of P:1247-1248) and costs O(m) — nothing
 // proportional to n is touched.  Out-of-range targets are
-// skipped and their vs_bar is 0 (reading R4).  VJP_ACCUMULATE applies to
+// skipped and their vs_bar is 0 (reading R4).  vjp_scatter_forward /
+// vjp_scatter_restore are the in-place update's forward save and
+// the return sweep's step (3), O(m) as well.  VJP_ACCUMULATE applies to
 // vs_bar (the paper's +=); xs_bar is the assignment of P:1275.
 #include "common.cuh"
 
@@ -24,6 +26,27 @@ __global__ void scatter_vjp(const I *__restrict__ is, const T *ys_bar, T *xs_bar
         const T g = in ? ys_bar[t * width + c] : (T)0;
         vs_bar[k] = acc ? (T)((double)vs_bar[k] + (double)g) : g;
         if (in) xs_bar[t * width + c] = (T)0;  // after the gather (aliasing-safe)
+    }
+}
+
+// Forward save + in-place update: saved[j] = xs[is[j]] before
+// xs[is[j]] = vs[j], in the same thread.  RESTORE=true is the return sweep's
+// step (3): ys[is[j]] = saved[j].  Distinct targets make every
+// (target, component) owned by one thread.
+template <class T, class I, bool RESTORE>
+__global__ void scatter_save(const I *__restrict__ is, const T *__restrict__ vs, T *xs, T *__restrict__ saved,
+                             int64_t n, int64_t m, int64_t width) {
+    const int64_t total = m * width;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = k / width, c = k - j * width;
+        const int64_t t = (int64_t)is[j];
+        const bool in = t >= 0 && t < n;
+        if (RESTORE) {
+            if (in) xs[t * width + c] = saved[k];
+        } else {
+            saved[k] = in ? xs[t * width + c] : (T)0;
+            if (in) xs[t * width + c] = vs[k];
+        }
     }
 }
 
@@ -59,6 +82,29 @@ vjp_status run(int64_t n, int64_t m, int64_t width, const void *is, const void *
                                           static_cast<T *>(xsb), static_cast<T *>(vsb), n, m, width, acc);
     vjph::count_launch();
     return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+}
+
+template <class T, class I, bool RESTORE>
+vjp_status run_save(int64_t n, int64_t m, int64_t width, const void *is, const void *vs, void *xs, void *saved,
+                    cudaStream_t s) {
+    const int64_t total = m * width;
+    int64_t g = (total + 255) / 256;
+    const int64_t cap = (int64_t)vjph::sm_count() * 16;
+    int grid = (int)(g < 1 ? 1 : (g > cap ? cap : g));
+    scatter_save<T, I, RESTORE><<<grid, 256, 0, s>>>(static_cast<const I *>(is), static_cast<const T *>(vs),
+                                                     static_cast<T *>(xs), static_cast<T *>(saved), n, m, width);
+    vjph::count_launch();
+    return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+}
+
+template <bool RESTORE>
+vjp_status dispatch_save(vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, int64_t width, const void *is,
+                         const void *vs, void *xs, void *saved, cudaStream_t s) {
+    if (dtype == VJP_F64)
+        return itype == VJP_I32 ? run_save<double, int32_t, RESTORE>(n, m, width, is, vs, xs, saved, s)
+                                : run_save<double, int64_t, RESTORE>(n, m, width, is, vs, xs, saved, s);
+    return itype == VJP_I32 ? run_save<float, int32_t, RESTORE>(n, m, width, is, vs, xs, saved, s)
+                            : run_save<float, int64_t, RESTORE>(n, m, width, is, vs, xs, saved, s);
 }
 
 template <class I>
@@ -117,6 +163,38 @@ vjp_status vjp_scatter(vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, i
                                 : run<double, int64_t>(n, m, width, is, ys_bar, xs_bar, vs_bar, s, acc);
     return itype == VJP_I32 ? run<float, int32_t>(n, m, width, is, ys_bar, xs_bar, vs_bar, s, acc)
                             : run<float, int64_t>(n, m, width, is, ys_bar, xs_bar, vs_bar, s, acc);
+}
+
+vjp_status vjp_scatter_forward(vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, int64_t width,
+                               const void *is, const void *vs, void *xs, void *xs_saved, void *ws, size_t ws_bytes,
+                               vjp_stream_t stream, unsigned flags) {
+    if ((dtype != VJP_F32 && dtype != VJP_F64) || (itype != VJP_I32 && itype != VJP_I64)) return VJP_EINVAL;
+    if (n < 0 || m < 0 || width < 1 || (flags & ~(unsigned)VJP_CHECK_INDICES)) return VJP_EINVAL;
+    if (m > 0 && (!is || !vs || !xs_saved || (n > 0 && !xs))) return VJP_EINVAL;
+    const void *ps[4] = {is, vs, xs, xs_saved};
+    for (const void *p : ps)
+        if (p && !vjph::aligned16(p)) return VJP_EALIGN;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (flags & VJP_CHECK_INDICES) {
+        if (!ws || ws_bytes < check_bytes(n)) return VJP_EWORKSPACE;
+        vjp_status st = itype == VJP_I32 ? check<int32_t>(n, m, is, ws, s) : check<int64_t>(n, m, is, ws, s);
+        if (st != VJP_OK) return st;
+    }
+    if (m == 0) return VJP_OK;
+    return dispatch_save<false>(dtype, itype, n, m, width, is, vs, xs, xs_saved, s);
+}
+
+vjp_status vjp_scatter_restore(vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, int64_t width,
+                               const void *is, const void *xs_saved, void *ys, vjp_stream_t stream) {
+    if ((dtype != VJP_F32 && dtype != VJP_F64) || (itype != VJP_I32 && itype != VJP_I64)) return VJP_EINVAL;
+    if (n < 0 || m < 0 || width < 1) return VJP_EINVAL;
+    if (m > 0 && (!is || !xs_saved || (n > 0 && !ys))) return VJP_EINVAL;
+    const void *ps[3] = {is, xs_saved, ys};
+    for (const void *p : ps)
+        if (p && !vjph::aligned16(p)) return VJP_EALIGN;
+    if (m == 0) return VJP_OK;
+    return dispatch_save<true>(dtype, itype, n, m, width, is, nullptr, ys, const_cast<void *>(xs_saved),
+                               reinterpret_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -31,6 +31,8 @@ for op in ('add', 'mul', 'min', 'max'):
 is_, yb = synth.scatter_inputs(10_000, 3000, device=dev)
 vjp.scatter(is_, yb)
 vjp.scatter(is_, yb.clone(), in_place=True)
+xs_ = yb.clone()
+vjp.scatter_restore(xs_, is_, vjp.scatter_forward(xs_, is_, yb[:3000].clone(), check=True))
 for op in ('linrec', 'mat2'):  # general reduce rule (YL kernels)
     w = vjp.WIDTH[vjp.OPS[op]]
     for n in (1, 1000, 70_001):
