@@ -350,7 +350,31 @@ def run_extra(args):
     dev = torch.device("cuda", 0)
     vjp.lib()
     peak, peak_src = peaks()
-    cases = []
+    def run_case(name, n, nbytes, fn):
+        # each case runs as soon as it is defined, so its inputs can be freed
+        # before the next case allocates
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = statistics.median(ts)
+        print(json.dumps({"extra": name, "n": n, "ms": ms, "elements_per_s": n / (ms * 1e-3),
+                          "alg_bytes": nbytes, "alg_gbs": nbytes / (ms * 1e-3) / 1e9,
+                          "frac_of_peak": nbytes / (ms * 1e-3) / 1e9 / peak, "peak": peak,
+                          "min_ms": min(ts)}), flush=True)
+
+    class _Cases:
+        def append(self, case):
+            run_case(*case)
+
+    cases = _Cases()
     N30, N28, N26 = 1 << 30, 1 << 28, 1 << 26
     w = args.workload
     if w in ("scan_add", "all"):
@@ -362,11 +386,19 @@ def run_extra(args):
                       lambda yb=yb, out=out: vjp.scan("add", yb, out=out, chunked=True)))
         cases.append(("scan ADD f64 n=2^30 look-back kernels", N30, 16 * N30,
                       lambda yb=yb, out=out: vjp.scan("add", yb, out=out, lookback=True)))
+        yb = out = None
+        yf = synth.scan_add_seed(N30, device=dev).float()
+        of = torch.empty_like(yf)
+        cases.append(("scan ADD f32 n=2^30 (8 B/elem)", N30, 8 * N30,
+                      lambda yf=yf, of=of: vjp.scan("add", yf, out=of)))
+        yf = of = None
+    yb = out = None
     if w in ("scan_linrec30", "all"):
         a, yb2 = synth.linrec_inputs(N30, device=dev)
         out2 = torch.empty_like(yb2)
         cases.append(("scan LINREC f64 n=2^30", N30, 64 * N30,
                       lambda yb2=yb2, a=a, out2=out2: vjp.scan("linrec", yb2, a, out=out2)))
+    a = yb2 = out2 = None
     if w in ("reduce", "all"):
         for z in ("none", "one", "two", "sparse"):
             a = synth.mul_inputs(N30, zeros=z, dtype=torch.float32, device=dev)
@@ -389,19 +421,30 @@ def run_extra(args):
         vs = torch.empty(1 << 24, dtype=torch.float64, device=dev)
         cases.append(("scatter in place f64 n=2^28 m=2^24 (32 B/target)", 1 << 24, 32 * (1 << 24),
                       lambda is_=is_, ybs=ybs, vs=vs: vjp.scatter(is_, ybs, in_place=True, vs_out=vs)))
+        # the in-place update's forward save + restore: per target
+        # index 8 B, xs read 8 B, xs_saved 8 B written, vs 8 B read, xs 8 B written;
+        # then restore: index 8 B, xs_saved 8 B, xs 8 B
+        saved = torch.empty(1 << 24, dtype=torch.float64, device=dev)
+        cases.append(("scatter forward save + restore f64 n=2^28 m=2^24 (64 B/target)", 1 << 24, 64 * (1 << 24),
+                      lambda is_=is_, ybs=ybs, vs=vs, saved=saved: vjp.scatter_restore(
+                          ybs, is_, vjp.scatter_forward(ybs, is_, vs, saved_out=saved))))
         # MIN scan (pick-left subgradient; the reverse maps need rs: K_F + K_R' + K_C)
         am = synth.min_inputs(N26, dtype=torch.float64, device=dev)
         ym = synth.uniform(N26, 10, device=dev)
         omn = torch.empty_like(ym)
         cases.append(("scan MIN f64 n=2^26 (chunked rs-dependent path, 24 B/elem method)", N26, 24 * N26,
                       lambda am=am, ym=ym, omn=omn: vjp.scan("min", ym, am, out=omn)))
+    o = am = ym = omn = is_ = ybs = vs = None
     if w in ("rbi", "all"):
-        for m in (1000, 1_000_000):
-            for op, nb in (("add", 12), ("mul", 32), ("max", 20)):
-                inds, a, hb = synth.rbi_inputs(N28, m, op, device=dev)
-                o = torch.empty(N28, dtype=torch.float64, device=dev)
-                cases.append((f"rbi {op.upper()} f64 n=2^28 m={m}", N28, nb * N28,
-                              (lambda op=op, inds=inds, a=a, hb=hb, o=o: vjp.reduce_by_index(op, inds, a, hb, out=o))))
+        for skew in (False, True):  # bins uniform over m, or skewed (floor(m u^2): a heavy head)
+            for m in (1000, 1_000_000):
+                for op, nb in (("add", 12), ("mul", 32), ("max", 20)):
+                    inds = a = hb = None
+                    inds, a, hb = synth.rbi_inputs(N28, m, op, device=dev, skew=skew)
+                    o = torch.empty(N28, dtype=torch.float64, device=dev)
+                    cases.append((f"rbi {op.upper()} f64 n=2^28 m={m}{' skewed bins' if skew else ''}", N28, nb * N28,
+                                  (lambda op=op, inds=inds, a=a, hb=hb, o=o: vjp.reduce_by_index(op, inds, a, hb, out=o))))
+        inds = a = hb = o = None
     if w in ("batched", "all"):
         # vectorised scans: ADD 2^20 x 64, LINREC 2^20 x 32 (f64)
         ya = synth.scan_add_seed((1 << 20) * 64, device=dev)
@@ -426,23 +469,6 @@ def run_extra(args):
         out = vjp.kmeans(P, C, 1.0)
         cases.append((f"kmeans grad n=1e6 k=1024 d=64 f64 (flops {2 * nk * kk * dk:.3g})", nk,
                       nk * dk * 8 * 2, lambda P=P, C=C, out=out: vjp.kmeans(P, C, 1.0, out=out)))
-    for name, n, nbytes, fn in cases:
-        for _ in range(args.warmup):
-            fn()
-        torch.cuda.synchronize()
-        ts = []
-        for _ in range(args.steps):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            fn()
-            e1.record()
-            e1.synchronize()
-            ts.append(e0.elapsed_time(e1))
-        ms = statistics.median(ts)
-        print(json.dumps({"extra": name, "n": n, "ms": ms, "elements_per_s": n / (ms * 1e-3),
-                          "alg_bytes": nbytes, "alg_gbs": nbytes / (ms * 1e-3) / 1e9,
-                          "frac_of_peak": nbytes / (ms * 1e-3) / 1e9 / peak, "peak": peak,
-                          "min_ms": min(ts)}), flush=True)
     return 0
 
 

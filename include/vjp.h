@@ -95,7 +95,7 @@ enum {
     VJP_SCAN_SWEEP = 1u << 17,    /* single GPU: the one-read L2-round sweep (one persistent
                                     kernel, as/ys_bar read from HBM once, each round re-read
                                     from L2) for any of ADD/MUL/LINREC/MAT2; it is already the
-                                    default for ADD without ys */
+                                    default for f64 ADD without ys */
     VJP_SCAN_CHUNKED = 1u << 18   /* tuning/testing: force the two chunked kernels */
 };
 

@@ -284,14 +284,16 @@ struct ScanImpl {
     static constexpr int SW_S_1 = 4;  // TMA stages when a stage is one 16 KB buffer
     static constexpr int SW_S_2 = 3;  // ... two or three buffers
 
-    // the one-read sweep is the default for scan(+) without ys on one GPU (its
-    // reverse maps commute: 3.74 vs 4.10 ms at 2^30 f64); the other operators
+    // the one-read sweep is the default for f64 scan(+) without ys on one GPU
+    // (its reverse maps commute: 3.73 vs 4.14 ms at 2^30 f64; for f32 the
+    // chunked kernels are faster, 2.20 vs 2.78 ms at 2^30); the other operators
     // take it only on request (their shuffle scans of d-vector maps make it
     // slower than the chunked kernels)
     static bool use_sweep(const ScanCall &c) {
         if (c.world != 1 || (c.flags & (VJP_SCAN_LOOKBACK | VJP_SCAN_CHUNKED))) return false;
         if (c.flags & VJP_SCAN_SWEEP) return true;
-        return std::is_same<Op, vjpk::OpAdd>::value && c.ys == nullptr && env_int("VJP_SCAN_NO_SWEEP", 0) == 0;
+        return std::is_same<Op, vjpk::OpAdd>::value && sizeof(T) == 8 && c.ys == nullptr &&
+               env_int("VJP_SCAN_NO_SWEEP", 0) == 0;
     }
 
     template <bool FWD, bool ACC, bool YS>
