@@ -444,6 +444,15 @@ def run_extra(args):
                     o = torch.empty(N28, dtype=torch.float64, device=dev)
                     cases.append((f"rbi {op.upper()} f64 n=2^28 m={m}{' skewed bins' if skew else ''}", N28, nb * N28,
                                   (lambda op=op, inds=inds, a=a, hb=hb, o=o: vjp.reduce_by_index(op, inds, a, hb, out=o))))
+            # the general rule: counting sort + per-bin product scans
+            if not skew:
+                for m in (1000, 1_000_000):
+                    inds = a = hb = None
+                    inds, a, hb = synth.rbi_inputs(N28, m, "mul", device=dev)
+                    o = torch.empty(N28, dtype=torch.float64, device=dev)
+                    cases.append((f"rbi MUL f64 n=2^28 m={m} general rule (sort + segmented scans)", N28, 32 * N28,
+                                  (lambda inds=inds, a=a, hb=hb, o=o: vjp.reduce_by_index("mul", inds, a, hb, out=o,
+                                                                                          general=True))))
         inds = a = hb = o = None
     if w in ("batched", "all"):
         # vectorised scans: ADD 2^20 x 64, LINREC 2^20 x 32 (f64)

@@ -251,6 +251,24 @@ vjp_status vjp_reduce_by_index(vjp_op op, vjp_dtype dtype, vjp_itype itype, int6
                                void *as_bar, void *hs, int64_t *winners, void *ws,
                                size_t ws_bytes, vjp_stream_t stream, unsigned flags);
 
+/* vjp_reduce_by_index_general — the paper's GENERAL rule for reduce_by_index
+ * (sec 5.1.2: "radix sort + segmented scans", left "work in
+ * progress" there), for MUL: per bin b, as_bar_i (+)= hs_bar[b] * l_i * r_i
+ * with l_i / r_i the product of the bin's other elements before / after i
+ * (the reduce rule of P:986-1013 per bin).  Counting sort by bin, then one
+ * warp per bin runs the forward and backward exclusive product scans.  Same
+ * arguments as vjp_reduce_by_index without the primal outputs; op must be
+ * VJP_MUL (ADD / MIN / MAX: VJP_EUNSUPPORTED — their special cases ARE the
+ * general rule); flags: VJP_ACCUMULATE only.  Domain: the partial products
+ * stay finite and normal (the special-case path tracks exponents instead).
+ * Out-of-range bins: as_bar 0 (R4).  Workspace (n + m) * 24 bytes-ish, from
+ * the query.  Results equal vjp_reduce_by_index(VJP_MUL) up to rounding. */
+size_t vjp_reduce_by_index_general_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_t n, int64_t m);
+vjp_status vjp_reduce_by_index_general(vjp_op op, vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m,
+                                       const void *inds, const void *as, const void *hs_bar,
+                                       void *as_bar, void *ws, size_t ws_bytes, vjp_stream_t stream,
+                                       unsigned flags);
+
 /* Multi-GPU split (partition by input range; per-bin state all-reduced):
  *   partial: per-bin state of the local shard into bin_val (DEVICE double[m])
  *            and bin_aux (DEVICE int64[m]):

@@ -80,6 +80,8 @@ def lib():
             "vjp_reduce_by_index_finish": ([ci, ci, ci, i64, i64, vp, vp, vp, vp, vp, vp, vp, sz, sp, vp, u32], ci),
             "vjp_scatter_workspace_bytes": ([ci, i64, i64], sz),
             "vjp_scatter": ([ci, ci, i64, i64, i64, vp, vp, vp, vp, vp, sz, vp, u32], ci),
+            "vjp_reduce_by_index_general_workspace_bytes": ([ci, ci, i64, i64], sz),
+            "vjp_reduce_by_index_general": ([ci, ci, ci, i64, i64, vp, vp, vp, vp, vp, sz, vp, u32], ci),
             "vjp_scatter_forward": ([ci, ci, i64, i64, i64, vp, vp, vp, vp, vp, sz, vp, u32], ci),
             "vjp_scatter_restore": ([ci, ci, i64, i64, i64, vp, vp, vp, vp], ci),
             "vjp_kmeans_workspace_bytes": ([ci, i64, i64, i64], sz),
@@ -271,10 +273,13 @@ def reduce(op, as_: torch.Tensor, y_bar, *, out: torch.Tensor | None = None, wan
 
 
 def reduce_by_index(op, inds: torch.Tensor, as_: torch.Tensor | None, hs_bar: torch.Tensor, *,
-                    out: torch.Tensor | None = None, want_hs: bool = False, accumulate: bool = False):
+                    out: torch.Tensor | None = None, want_hs: bool = False, accumulate: bool = False,
+                    general: bool = False):
     """as_bar of ``hs = reduce_by_index op m inds as_`` with m = len(hs_bar)
     (sec 5.1.2).  Returns as_bar, or (as_bar, hs, winners) if want_hs
-    (winners: MIN/MAX per-bin winner index, -1 for an empty bin; MUL: zero count)."""
+    (winners: MIN/MAX per-bin winner index, -1 for an empty bin; MUL: zero count).
+    general=True (MUL only): the paper's general rule, counting sort + per-bin
+    exclusive product scans (vjp_reduce_by_index_general)."""
     o = _op(op)
     host = not inds.is_cuda
     dev = _dev_of(inds, as_, hs_bar, out)
@@ -288,6 +293,18 @@ def reduce_by_index(op, inds: torch.Tensor, as_: torch.Tensor | None, hs_bar: to
     hs = torch.empty(m, dtype=hb.dtype, device=dev) if want_hs else None
     win = torch.empty(m, dtype=torch.int64, device=dev) if want_hs else None
     L = lib()
+    if general:
+        if want_hs:
+            raise ValueError("general=True returns the adjoint only")
+        ws = workspace(L.vjp_reduce_by_index_general_workspace_bytes(o, _dt(hb), n, m), dev)
+        _check(L.vjp_reduce_by_index_general(o, _dt(hb), _it(ix), n, m, _p(ix), _p(a), _p(hb), _p(ab), _p(ws),
+                                             0 if ws is None else ws.numel(), _stream(dev),
+                                             ACCUMULATE if accumulate else 0), "vjp_reduce_by_index_general")
+        if out is not None and not out.is_cuda:
+            out.copy_(ab, non_blocking=True)
+            torch.cuda.current_stream(dev).synchronize()
+            return out
+        return _host_out(ab, host)
     ws = workspace(L.vjp_reduce_by_index_workspace_bytes(o, _dt(hb), n, m), dev)
     _check(L.vjp_reduce_by_index(o, _dt(hb), _it(ix), n, m, _p(ix), _p(a), _p(hb), _p(ab), _p(hs), _p(win),
                                  _p(ws), 0 if ws is None else ws.numel(), _stream(dev),

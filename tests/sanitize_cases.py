@@ -28,6 +28,8 @@ for op in ('add', 'mul', 'min', 'max'):
         inds, a, hb = synth.rbi_inputs(n, m, op, device=dev)
         vjp.reduce_by_index(op, inds, a, hb, want_hs=True)
         vjp.reduce_by_index(op, inds, a, hb, out=torch.zeros_like(a), accumulate=True)
+        if op == 'mul':
+            vjp.reduce_by_index(op, inds, a, hb, general=True)
 is_, yb = synth.scatter_inputs(10_000, 3000, device=dev)
 vjp.scatter(is_, yb)
 vjp.scatter(is_, yb.clone(), in_place=True)

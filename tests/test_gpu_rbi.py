@@ -122,3 +122,36 @@ def test_rbi_mul_log2_accuracy():
     ulp = np.spacing(np.abs(ref)) + np.where(ref == 0, 5e-324, 0)
     err = np.abs(got - ref) / ulp
     assert float(err.max()) <= 2.0, float(err.max())
+
+
+@pytest.mark.parametrize("it", [torch.int32, torch.int64], ids=["i32", "i64"])
+@pytest.mark.parametrize("dt", [np.float64, np.float32], ids=["f64", "f32"])
+def test_rbi_mul_general_rule(dt, it):
+    """vjp_reduce_by_index_general (counting sort + per-bin
+    exclusive product scans) vs the oracle (whose per-bin l_i r_i is the same
+    rule, computed sequentially in index order): zeros per bin 0 / 1 / >= 2
+    (synth: Poisson(1) zeros per bin), out-of-range bins, one bin, skew."""
+    for n, m, skew in [(1, 1, False), (5, 3, False), (1000, 1, False), (4097, 17, False), (100_003, 1000, False),
+                       (300_001, 20_000, True), (1 << 20, 1_000_000, False)]:
+        inds, a, hb = synth.rbi_inputs(n, m, "mul", dtype=TD[dt], itype=it, skew=skew)
+        if n > 4:
+            inds[1] = -1
+            inds[3] = m + 5
+        ref = oracle.vjp_reduce_by_index("mul", inds.numpy(), a.numpy(), hb.numpy())[0]
+        got = vjp.reduce_by_index("mul", inds.to(DEV), a.to(DEV), hb.to(DEV), general=True)
+        assert_close(got.cpu().numpy(), ref, dt, what=f"rbi mul general n={n} m={m}")
+        if n > 4:
+            assert float(got[1]) == 0.0 and float(got[3]) == 0.0
+
+
+def test_rbi_mul_general_accumulate_and_unsupported():
+    inds, a, hb = synth.rbi_inputs(50_000, 300, "mul")
+    base = synth.uniform(50_000, 33)
+    ref = oracle.vjp_reduce_by_index("mul", inds.numpy(), a.numpy(), hb.numpy(), out=base.numpy().copy(),
+                                     accumulate=True)[0]
+    out = base.to(DEV)
+    vjp.reduce_by_index("mul", inds.to(DEV), a.to(DEV), hb.to(DEV), out=out, accumulate=True, general=True)
+    assert_close(out.cpu().numpy(), ref, np.float64, what="general accumulate")
+    with pytest.raises(vjp.VjpError) as e:
+        vjp.reduce_by_index("add", inds.to(DEV), a.to(DEV), hb.to(DEV), general=True)
+    assert e.value.code == 2
