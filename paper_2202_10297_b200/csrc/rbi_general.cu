@@ -7,12 +7,15 @@
 // l_i / r_i = product of the bin's other elements before / after i.  Here:
 //   rg_count   per-bin element counts (global 64-bit reductions)
 //   rg_offsets exclusive scan of the counts (one CTA) -> bin segments
-//   rg_place   bucket the elements into their bin's segment (counting sort;
+//   rg_place   bucket the values into their bin's segment and record each
+//              element's slot pos_of[i] (counting sort;
 //              the order inside a segment is the atomic order — l_i * r_i is
 //              the product of the OTHER elements whatever the order, so only
 //              rounding depends on it)
 //   rg_bins    one warp per bin: forward exclusive product scan (l, stored),
-//              backward exclusive product scan (r), as_bar[i] = hbar * l * r
+//              backward exclusive product scan (r), res = hbar * l * r in
+//              segment order
+//   rg_gather  as_bar[i] = res[pos_of[i]] in index order
 // Small m (<= 8192 bins, n / m long segments): per-chunk shared-memory
 // histograms + a column scan give each (chunk, bin) its output range, the
 // placement uses shared-memory cursors (runs of a bin are contiguous), and
@@ -72,16 +75,15 @@ __global__ void rg_offsets(const unsigned long long *__restrict__ cnt, int64_t m
 
 template <class T, class I>
 __global__ void rg_place(const I *__restrict__ inds, const T *__restrict__ as, int64_t n, int64_t m,
-                         unsigned long long *cursor, int64_t *perm, double *val, T *as_bar, int acc) {
+                         unsigned long long *cursor, int64_t *pos_of, double *val) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b = (int64_t)inds[i];
+        int64_t pos = -1;  // out-of-range bin: no contribution (reading R4)
         if (b >= 0 && b < m) {
-            const unsigned long long pos = atomicAdd(cursor + b, 1ull);
-            perm[pos] = i;
+            pos = (int64_t)atomicAdd(cursor + b, 1ull);
             val[pos] = (double)as[i];
-        } else if (!acc) {
-            as_bar[i] = (T)0;  // out-of-range bin: no contribution (reading R4)
         }
+        pos_of[i] = pos;
     }
 }
 
@@ -112,8 +114,7 @@ __device__ __forceinline__ double warp_excl_prod_rev(double v, int lane, double 
 
 template <class T>
 __global__ void rg_bins(const unsigned long long *__restrict__ off, const unsigned long long *__restrict__ cnt,
-                        int64_t m, const int64_t *__restrict__ perm, const double *__restrict__ val, double *lbuf,
-                        const T *__restrict__ hs_bar, T *as_bar, int acc) {
+                        int64_t m, const double *__restrict__ val, double *lbuf, const T *__restrict__ hs_bar) {
     const int lane = threadIdx.x & 31;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -140,9 +141,7 @@ __global__ void rg_bins(const unsigned long long *__restrict__ off, const unsign
             double tot;
             const double e = warp_excl_prod_rev(v, lane, &tot);
             if (k < len) {
-                const double g = hb * (lbuf[s0 + k] * (e * carry));
-                const int64_t i = perm[s0 + k];
-                as_bar[i] = acc ? (T)((double)as_bar[i] + g) : (T)g;
+                lbuf[s0 + k] = hb * (lbuf[s0 + k] * (e * carry));  // the adjoint, in segment order
             }
             carry *= tot;
         }
@@ -187,8 +186,7 @@ __global__ void rg_colscan_small(const unsigned *__restrict__ H, int64_t nchunks
 
 template <class T, class I>
 __global__ void rg_place_small(const I *__restrict__ inds, const T *__restrict__ as, int64_t n, int64_t m,
-                               const unsigned long long *__restrict__ base, int64_t *perm, double *val, T *as_bar,
-                               int acc) {
+                               const unsigned long long *__restrict__ base, int64_t *pos_of, double *val) {
     extern __shared__ __align__(16) unsigned char sm_[];
     unsigned long long *bs = reinterpret_cast<unsigned long long *>(sm_);
     unsigned *lc = reinterpret_cast<unsigned *>(bs + m);
@@ -197,13 +195,12 @@ __global__ void rg_place_small(const I *__restrict__ inds, const T *__restrict__
     const int64_t e0 = (int64_t)blockIdx.x * kGenChunk, e1 = min(n, e0 + kGenChunk);
     for (int64_t i = e0 + threadIdx.x; i < e1; i += blockDim.x) {
         const int64_t b = (int64_t)inds[i];
+        int64_t pos = -1;
         if (b >= 0 && b < m) {
-            const unsigned long long pos = bs[b] + atomicAdd(lc + b, 1u);
-            perm[pos] = i;
+            pos = (int64_t)(bs[b] + atomicAdd(lc + b, 1u));
             val[pos] = (double)as[i];
-        } else if (!acc) {
-            as_bar[i] = (T)0;
         }
+        pos_of[i] = pos;
     }
 }
 
@@ -212,8 +209,8 @@ __global__ void rg_place_small(const I *__restrict__ inds, const T *__restrict__
 template <class T>
 __global__ void __launch_bounds__(1024) rg_bins_cta(const unsigned long long *__restrict__ off,
                                                     const unsigned long long *__restrict__ cnt, int64_t m,
-                                                    const int64_t *__restrict__ perm, const double *__restrict__ val,
-                                                    double *lbuf, const T *__restrict__ hs_bar, T *as_bar, int acc) {
+                                                    const double *__restrict__ val, double *lbuf,
+                                                    const T *__restrict__ hs_bar) {
     __shared__ double part[32], pre[32], suf[32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int64_t b = blockIdx.x; b < m; b += gridDim.x) {
@@ -252,9 +249,7 @@ __global__ void __launch_bounds__(1024) rg_bins_cta(const unsigned long long *__
                 double tot;
                 const double e = warp_excl_prod_rev(v, lane, &tot);
                 if (k < p1) {
-                    const double g = hb * (lbuf[s0 + k] * (e * carry));
-                    const int64_t i = perm[s0 + k];
-                    as_bar[i] = acc ? (T)((double)as_bar[i] + g) : (T)g;
+                    lbuf[s0 + k] = hb * (lbuf[s0 + k] * (e * carry));
                 }
                 carry *= tot;
             }
@@ -263,12 +258,24 @@ __global__ void __launch_bounds__(1024) rg_bins_cta(const unsigned long long *__
     }
 }
 
+// write-back in index order: as_bar[i] (+)= res[pos_of[i]] (coalesced stores,
+// random 8-byte reads, instead of a random read-modify-write scatter)
+template <class T>
+__global__ void rg_gather(const int64_t *__restrict__ pos_of, const double *__restrict__ res, int64_t n, T *as_bar,
+                          int acc) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = pos_of[i];
+        const double g = p >= 0 ? res[p] : 0.0;
+        as_bar[i] = acc ? (T)((double)as_bar[i] + g) : (T)g;
+    }
+}
+
 }  // namespace vjpk
 
 namespace {
 
 struct GLayout {
-    size_t cnt, off, cur, perm, val, lbuf, H, base, total;
+    size_t cnt, off, cur, pos, val, lbuf, H, base, total;
 };
 GLayout glayout(int64_t n, int64_t m) {
     GLayout L{};
@@ -277,7 +284,7 @@ GLayout glayout(int64_t n, int64_t m) {
     L.cnt = take(8 * (size_t)m);
     L.off = take(8 * (size_t)m);
     L.cur = take(8 * (size_t)m);
-    L.perm = take(8 * (size_t)n);
+    L.pos = take(8 * (size_t)n);
     L.val = take(8 * (size_t)n);
     L.lbuf = take(8 * (size_t)n);
     if (m <= vjpk::kGenSmallM) {
@@ -302,7 +309,7 @@ vjp_status run_general(int64_t n, int64_t m, const void *inds_, const void *as_,
     auto *cnt = reinterpret_cast<unsigned long long *>(w + L.cnt);
     auto *off = reinterpret_cast<unsigned long long *>(w + L.off);
     auto *cur = reinterpret_cast<unsigned long long *>(w + L.cur);
-    auto *perm = reinterpret_cast<int64_t *>(w + L.perm);
+    auto *pos_of = reinterpret_cast<int64_t *>(w + L.pos);
     auto *val = reinterpret_cast<double *>(w + L.val);
     auto *lbuf = reinterpret_cast<double *>(w + L.lbuf);
     if (cudaMemsetAsync(cnt, 0, 8 * (size_t)m, s) != cudaSuccess) return VJP_ECUDA;
@@ -319,19 +326,21 @@ vjp_status run_general(int64_t n, int64_t m, const void *inds_, const void *as_,
         rg_hist_small<I><<<(unsigned)nch, 1024, smh, s>>>(inds, n, m, H, cnt);
         rg_offsets<<<1, 1024, 0, s>>>(cnt, m, off, cur);
         rg_colscan_small<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(H, nch, m, off, base);
-        rg_place_small<T, I><<<(unsigned)nch, 1024, smp, s>>>(inds, as, n, m, base, perm, val, ab, acc);
+        rg_place_small<T, I><<<(unsigned)nch, 1024, smp, s>>>(inds, as, n, m, base, pos_of, val);
         const int64_t gcap = (int64_t)vjph::sm_count() * 2;
-        rg_bins_cta<T><<<(unsigned)(m < gcap ? m : gcap), 1024, 0, s>>>(off, cnt, m, perm, val, lbuf, hsb, ab, acc);
+        rg_bins_cta<T><<<(unsigned)(m < gcap ? m : gcap), 1024, 0, s>>>(off, cnt, m, val, lbuf, hsb);
         vjph::count_launch(5);
     } else {
         rg_count<I><<<grid, 256, 0, s>>>(inds, n, m, cnt);
         rg_offsets<<<1, 1024, 0, s>>>(cnt, m, off, cur);
-        rg_place<T, I><<<grid, 256, 0, s>>>(inds, as, n, m, cur, perm, val, ab, acc);
+        rg_place<T, I><<<grid, 256, 0, s>>>(inds, as, n, m, cur, pos_of, val);
         int64_t gb = (m * 32 + 255) / 256;
         const int gridb = (int)(gb < 1 ? 1 : (gb > cap ? cap : gb));
-        rg_bins<T><<<gridb, 256, 0, s>>>(off, cnt, m, perm, val, lbuf, hsb, ab, acc);
+        rg_bins<T><<<gridb, 256, 0, s>>>(off, cnt, m, val, lbuf, hsb);
         vjph::count_launch(4);
     }
+    rg_gather<T><<<grid, 256, 0, s>>>(pos_of, lbuf, n, ab, acc);
+    vjph::count_launch();
     return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
 }
 
