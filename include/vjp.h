@@ -322,6 +322,19 @@ vjp_status vjp_scatter(vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, i
                        const void *is, const void *ys_bar, void *xs_bar, void *vs_bar, void *ws,
                        size_t ws_bytes, vjp_stream_t stream, unsigned flags);
 
+/* vjp_scatter_shard — multi-GPU split of vjp_scatter (sec 5.3): ys_bar is
+ * partitioned contiguously, this rank owns global elements [global_offset,
+ * global_offset + n_local); `is` holds the m GLOBAL targets (replicated).
+ * The call zeroes the owned targets of xs_bar (in place when xs_bar aliases
+ * ys_bar: O(m)) and writes vs_bar_partial[j] = ys_bar[is[j] - global_offset]
+ * for owned targets, 0 otherwise; the caller SUMs vs_bar_partial over the
+ * ranks (exactly one rank owns each in-range target, so the sum is exact) —
+ * one all_reduce of m * width scalars (paper_2202_10297_b200.dist.scatter).
+ * No flags (accumulate / index checks are the caller's, after the sum). */
+vjp_status vjp_scatter_shard(vjp_dtype dtype, vjp_itype itype, int64_t n_local, int64_t m, int64_t width,
+                             const void *is, const void *ys_bar, void *xs_bar, void *vs_bar_partial,
+                             const vjp_shard *shard, vjp_stream_t stream);
+
 /* ======================================================================
  * vjp_scatter_forward / vjp_scatter_restore — the in-place scatter's forward
  * save and the return sweep's step (3) (sec 5.3)

@@ -82,6 +82,7 @@ def lib():
             "vjp_scatter": ([ci, ci, i64, i64, i64, vp, vp, vp, vp, vp, sz, vp, u32], ci),
             "vjp_reduce_by_index_general_workspace_bytes": ([ci, ci, i64, i64], sz),
             "vjp_reduce_by_index_general": ([ci, ci, ci, i64, i64, vp, vp, vp, vp, vp, sz, vp, u32], ci),
+            "vjp_scatter_shard": ([ci, ci, i64, i64, i64, vp, vp, vp, vp, sp, vp], ci),
             "vjp_scatter_forward": ([ci, ci, i64, i64, i64, vp, vp, vp, vp, vp, sz, vp, u32], ci),
             "vjp_scatter_restore": ([ci, ci, i64, i64, i64, vp, vp, vp, vp], ci),
             "vjp_kmeans_workspace_bytes": ([ci, i64, i64, i64], sz),

@@ -17,11 +17,11 @@ namespace vjpk {
 
 template <class T, class I>
 __global__ void scatter_vjp(const I *__restrict__ is, const T *ys_bar, T *xs_bar, T *__restrict__ vs_bar, int64_t n,
-                            int64_t m, int64_t width, int acc) {
+                            int64_t m, int64_t width, int acc, int64_t goff) {
     const int64_t total = m * width;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
         const int64_t j = k / width, c = k - j * width;
-        const int64_t t = (int64_t)is[j];
+        const int64_t t = (int64_t)is[j] - goff;  // goff: first global target this shard owns
         const bool in = t >= 0 && t < n;
         const T g = in ? ys_bar[t * width + c] : (T)0;
         vs_bar[k] = acc ? (T)((double)vs_bar[k] + (double)g) : g;
@@ -73,13 +73,13 @@ size_t check_bytes(int64_t n) { return 256 + vjph::align256((size_t)((n + 31) / 
 
 template <class T, class I>
 vjp_status run(int64_t n, int64_t m, int64_t width, const void *is, const void *ysb, void *xsb, void *vsb,
-               cudaStream_t s, int acc) {
+               cudaStream_t s, int acc, int64_t goff = 0) {
     const int64_t total = m * width;
     int64_t g = (total + 255) / 256;
     const int64_t cap = (int64_t)vjph::sm_count() * 16;
     int grid = (int)(g < 1 ? 1 : (g > cap ? cap : g));
     scatter_vjp<T, I><<<grid, 256, 0, s>>>(static_cast<const I *>(is), static_cast<const T *>(ysb),
-                                          static_cast<T *>(xsb), static_cast<T *>(vsb), n, m, width, acc);
+                                          static_cast<T *>(xsb), static_cast<T *>(vsb), n, m, width, acc, goff);
     vjph::count_launch();
     return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
 }
@@ -163,6 +163,34 @@ vjp_status vjp_scatter(vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, i
                                 : run<double, int64_t>(n, m, width, is, ys_bar, xs_bar, vs_bar, s, acc);
     return itype == VJP_I32 ? run<float, int32_t>(n, m, width, is, ys_bar, xs_bar, vs_bar, s, acc)
                             : run<float, int64_t>(n, m, width, is, ys_bar, xs_bar, vs_bar, s, acc);
+}
+
+vjp_status vjp_scatter_shard(vjp_dtype dtype, vjp_itype itype, int64_t n_local, int64_t m, int64_t width,
+                             const void *is, const void *ys_bar, void *xs_bar, void *vs_bar_partial,
+                             const vjp_shard *shard, vjp_stream_t stream) {
+    if (!shard || shard->world < 1 || shard->global_offset < 0 || n_local < 0 ||
+        shard->global_offset + n_local > shard->global_n)
+        return VJP_EINVAL;
+    if ((dtype != VJP_F32 && dtype != VJP_F64) || (itype != VJP_I32 && itype != VJP_I64)) return VJP_EINVAL;
+    if (m < 0 || width < 1) return VJP_EINVAL;
+    if ((m > 0 && (!is || !vs_bar_partial)) || (n_local > 0 && (!ys_bar || !xs_bar))) return VJP_EINVAL;
+    const void *ps[4] = {is, ys_bar, xs_bar, vs_bar_partial};
+    for (const void *p : ps)
+        if (p && !vjph::aligned16(p)) return VJP_EALIGN;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (n_local > 0 && xs_bar != ys_bar) {
+        const size_t es = dtype == VJP_F64 ? 8 : 4;
+        if (cudaMemcpyAsync(xs_bar, ys_bar, (size_t)n_local * (size_t)width * es, cudaMemcpyDeviceToDevice, s) !=
+            cudaSuccess)
+            return VJP_ECUDA;
+    }
+    if (m == 0) return VJP_OK;
+    const int64_t g = shard->global_offset;
+    if (dtype == VJP_F64)
+        return itype == VJP_I32 ? run<double, int32_t>(n_local, m, width, is, ys_bar, xs_bar, vs_bar_partial, s, 0, g)
+                                : run<double, int64_t>(n_local, m, width, is, ys_bar, xs_bar, vs_bar_partial, s, 0, g);
+    return itype == VJP_I32 ? run<float, int32_t>(n_local, m, width, is, ys_bar, xs_bar, vs_bar_partial, s, 0, g)
+                            : run<float, int64_t>(n_local, m, width, is, ys_bar, xs_bar, vs_bar_partial, s, 0, g);
 }
 
 vjp_status vjp_scatter_forward(vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, int64_t width,

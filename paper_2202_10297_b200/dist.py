@@ -14,6 +14,10 @@ exchange step:
   reduce_by_index per-bin state -> all_reduce (PRODUCT+SUM for *, MAX/MIN then
                   MIN of candidate indices for max/min) -> finish; ADD needs no
                   exchange (hs_bar is replicated).
+  scatter         ys_bar partitioned, targets replicated: each rank zeroes its
+                  own targets and gathers them into a partial vs_bar (0 for
+                  targets it does not own) -> all_reduce SUM (m * width
+                  scalars; exactly one owner per target, so the sum is exact).
   kmeans          (config 5) points partitioned by rank, centers replicated:
                   every output is a sum over points, so the per-rank partials
                   (centers_bar, Hessian diagonal, counts, cost) are all_reduced
@@ -168,6 +172,25 @@ def reduce_by_index(op, inds: torch.Tensor, as_: torch.Tensor | None, hs_bar: to
                                         _p(bin_aux), _p(ws), nbytes, sh, s, ACCUMULATE if accumulate else 0),
            "vjp_reduce_by_index_finish")
     return ab
+
+
+def scatter(is_: torch.Tensor, ys_bar: torch.Tensor, *, offset: int, global_n: int, width: int = 1,
+            in_place: bool = False, group=None):
+    """Adjoints of ys = scatter xs is vs with ys_bar partitioned by rank (this
+    rank: global elements [offset, offset + len(ys_bar) / width)); `is_` holds
+    the GLOBAL targets on every rank.  Returns (xs_bar_local, vs_bar) with
+    vs_bar complete on every rank."""
+    dev = ys_bar.device
+    ix = is_.to(dev)
+    n, m = ys_bar.numel() // width, ix.numel()
+    xb = ys_bar if in_place else torch.empty_like(ys_bar)
+    vb = torch.empty(m * width, dtype=ys_bar.dtype, device=dev)
+    sh = _shard(offset, n, global_n, group)
+    _check(lib().vjp_scatter_shard(_dt(ys_bar), _it(ix), n, m, width, _p(ix), _p(ys_bar), _p(xb), _p(vb), sh,
+                                   _stream(dev)), "vjp_scatter_shard")
+    if sh.world > 1:
+        _all_reduce(vb, dist.ReduceOp.SUM, group)
+    return xb, vb
 
 
 def kmeans(points: torch.Tensor, centers: torch.Tensor, cost_bar=1.0, *, group=None, hess: bool = True):

@@ -136,6 +136,20 @@ def _worker(rank, world, port, q):
         got = aux.numpy().copy()
         got[got == np.iinfo(np.int64).max] = -1
         assert np.array_equal(got, win_full)
+        # scatter with ys_bar partitioned (dist.scatter / vjp_scatter_shard): each
+        # rank gathers only the targets it owns (shifted to local indices, the
+        # others out of range -> 0), SUM all_reduce of vs_bar; xs_bar per slice
+        NS, MS = 50_021, 9_000
+        is_, ybs = synth.scatter_inputs(NS, MS, oob=3)
+        off, n = shard_bounds(NS, world, rank)
+        loc = is_.numpy() - off
+        loc = np.where((loc >= 0) & (loc < n), loc, n + 1)  # not owned: out of range (reading R4)
+        xb_loc, vb_loc, _ = oracle.vjp_scatter(loc, ybs.numpy()[off:off + n].copy())
+        vb = torch.from_numpy(vb_loc.copy())
+        dist.all_reduce(vb, op=dist.ReduceOp.SUM)
+        rx, rv, _ = oracle.vjp_scatter(is_.numpy(), ybs.numpy())
+        assert np.array_equal(vb.numpy(), rv)
+        assert np.array_equal(xb_loc, rx[off:off + n])
         dist.barrier()
         dist.destroy_process_group()
         q.put((rank, "ok"))

@@ -90,6 +90,20 @@ def _worker(rank, world, port, q):
             if rank == 0:
                 ref = oracle.vjp_reduce_by_index(op, inds.numpy(), a.numpy(), hb.numpy())[0]
                 assert_close(np.concatenate(parts), ref, np.float64, what=f"2-rank rbi {op}")
+        # scatter: ys_bar partitioned, global targets replicated, vs_bar all_reduced
+        for width in (1, 3):
+            N, M = 100_003, 30_000
+            off, n = vdist.shard_bounds(N, world, rank)
+            is_, yb = synth.scatter_inputs(N, M, oob=2)
+            yb = yb.repeat_interleave(width) if width > 1 else yb
+            xb, vb = vdist.scatter(is_.to(dev), yb[off * width:(off + n) * width].clone().to(dev), offset=off,
+                                   global_n=N, width=width, in_place=(width == 1))
+            parts = [None] * world
+            dist.all_gather_object(parts, xb.cpu().numpy())
+            if rank == 0:
+                rx, rv, _ = oracle.vjp_scatter(is_.numpy(), yb.numpy(), width=width)
+                assert np.array_equal(np.concatenate(parts), rx), "2-rank scatter xs_bar"
+                assert np.array_equal(vb.cpu().numpy(), rv), "2-rank scatter vs_bar"
         # config-5 k-means gradient: points split by rank, all_reduce of partials
         N, K, D = 40_003, 96, 24
         P, C = synth.kmeans_inputs(N, K, D)
