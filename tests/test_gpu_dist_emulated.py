@@ -200,3 +200,30 @@ def test_rbi_split_emulated(op, m, world):
         assert_close(got, ref, np.float64, what=f"split rbi mul m={m}")
     else:
         assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+@pytest.mark.parametrize("it", [torch.int32, torch.int64], ids=["i32", "i64"])
+def test_scatter_split_emulated(world, it):
+    """vjp_scatter_shard per shard (ragged contiguous split of ys_bar, global
+    targets replicated), the all_reduce SUM of the partial vs_bar emulated:
+    bit-exact against the oracle on the whole array (one owner per target)."""
+    L = vjp.lib()
+    N, M, width = 70_001, 20_000, 2
+    is_, yb = synth.scatter_inputs(N, M, itype=it, oob=4)
+    yb = yb.repeat_interleave(width)
+    rx, rv, _ = oracle.vjp_scatter(is_.numpy(), yb.numpy(), width=width)
+    ix = is_.to(DEV)
+    vsum = torch.zeros(M * width, dtype=torch.float64, device=DEV)
+    xparts = []
+    for r, (off, n) in enumerate(shards(N, world)):
+        ys_loc = yb[off * width:(off + n) * width].clone().to(DEV)
+        vpart = torch.empty(M * width, dtype=torch.float64, device=DEV)
+        sh = VjpShard(r, world, off, N)
+        rc = L.vjp_scatter_shard(2, 1 if it == torch.int32 else 2, n, M, width, _p(ix), _p(ys_loc), _p(ys_loc),
+                                 _p(vpart), sh, _s())
+        assert rc == 0
+        vsum += vpart
+        xparts.append(ys_loc.cpu().numpy())
+    assert np.array_equal(np.concatenate(xparts), rx)
+    assert np.array_equal(vsum.cpu().numpy(), rv)
