@@ -69,6 +69,12 @@ def test_golden(case, dt):
         assert rc == 0
         assert xb.tolist() == _arr(case["xs_bar"], dt).tolist()
         assert vb.tolist() == _arr(case["vs_bar"], dt).tolist()
+    elif k == "scatter_fwd":
+        ys, saved = oracle.scatter_forward(_arr(case["xs"], dt), np.array(case["is"], np.int64), _arr(case["vs"], dt))
+        assert ys.tolist() == _arr(case["ys"], dt).tolist()
+        assert saved.tolist() == _arr(case["xs_saved"], dt).tolist()
+        back = oracle.scatter_restore(ys, np.array(case["is"], np.int64), saved)
+        assert back.tolist() == _arr(case["xs"], dt).tolist()
     else:
         raise AssertionError(k)
 
