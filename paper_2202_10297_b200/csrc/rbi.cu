@@ -239,7 +239,16 @@ __device__ __forceinline__ double log2_abs(double x) {
         m *= 0.5;
         e += 1;
     }
-    const double s = (m - 1.0) / (m + 1.0);
+    // s = (m - 1) / (m + 1) without the IEEE division's special-case path
+    // (m + 1 in [1.7, 2.5): normal, no overflow): hardware reciprocal
+    // estimate, two Newton steps, one residual correction of the quotient
+    const double num = m - 1.0, den = m + 1.0;
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(den));
+    r = fma(r, fma(-den, r, 1.0), r);
+    r = fma(r, fma(-den, r, 1.0), r);
+    double s = num * r;
+    s = fma(r, fma(-s, den, num), s);
     const double s2 = s * s;
     double p = 1.0 / 23.0;
     p = fma(p, s2, 1.0 / 21.0);
