@@ -188,6 +188,27 @@ __device__ __forceinline__ typename Op::Map row_map(const unsigned char *sA, con
                                                     int64_t e0, bool mask, int64_t n,
                                                     const typename Op::Val *yl = nullptr) {
     using G = Geo<Op, T>;
+    if constexpr (std::is_same<Op, OpAdd>::value && !YL && sizeof(T) == 8) {
+        // + maps commute: one partial sum per access group (independent
+        // chains instead of 16 dependent adds per row), then a tree.  f64
+        // only: measured 3.73 -> 3.69 ms for the f64 sweep at 2^30, while the
+        // f32 chunked reduce got slower (2.19 -> 2.34 ms)
+        double part[G::NG];
+#pragma unroll
+        for (int g = 0; g < G::NG; ++g) {
+            uint32_t wy[G::GB / 4];
+            lds_group<G::GB>(sY, t, g, wy);
+            part[g] = 0.0;
+#pragma unroll
+            for (int e = 0; e < G::EG; ++e)
+                if (!mask || e0 + g * G::EG + e < n) part[g] += dec<T, 1>(wy + e * (G::ES / 4)).x[0];
+        }
+#pragma unroll
+        for (int w = 1; w < G::NG; w <<= 1)
+#pragma unroll
+            for (int g = 0; g + w < G::NG; g += 2 * w) part[g] += part[g + w];
+        return {part[0]};
+    }
     typename Op::Map Tm = Op::map_id();
 #pragma unroll
     for (int g = G::NG - 1; g >= 0; --g) {
