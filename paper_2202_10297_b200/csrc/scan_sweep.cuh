@@ -530,6 +530,43 @@ __global__ void __launch_bounds__(NT + 64, (FWD || ACC) ? 2 : 3) scan_sweep(cons
 #pragma unroll
                 for (int q = 0; q < G::EPR; ++q) rsp[q] = Op::fwd_id();
             }
+            if constexpr (std::is_same<Op, OpAdd>::value && !FWD && sizeof(T) == 8) {
+                // + (f64): group sums first, then the suffix over the groups,
+                // then inside each group — dependent chain NG + EG instead of EPR
+                double yv[G::EPR], gs[G::NG], gsuf[G::NG];
+#pragma unroll
+                for (int g = 0; g < G::NG; ++g) {
+                    uint32_t wy[G::GB / 4];
+                    lds_group<G::GB>(sY, t, g, wy);
+                    gs[g] = 0.0;
+#pragma unroll
+                    for (int e = 0; e < G::EG; ++e) {
+                        const int q = g * G::EG + e;
+                        yv[q] = (!last || e0 + q < p.n) ? dec<T, 1>(wy + e * (G::ES / 4)).x[0] : 0.0;
+                        gs[g] += yv[q];
+                    }
+                }
+                gsuf[G::NG - 1] = Xr.x[0];
+#pragma unroll
+                for (int g = G::NG - 2; g >= 0; --g) gsuf[g] = gsuf[g + 1] + gs[g + 1];
+#pragma unroll
+                for (int g = G::NG - 1; g >= 0; --g) {
+                    uint32_t wc[G::GB / 4], wo[G::GB / 4];
+                    if (ACC) lds_group<G::GB>(sC, t, g, wc);
+                    double run = gsuf[g];
+#pragma unroll
+                    for (int e = G::EG - 1; e >= 0; --e) {
+                        const int q = g * G::EG + e;
+                        run = yv[q] + run;
+                        V o;
+                        o.x[0] = run;
+                        if (ACC) o.x[0] += dec<T, 1>(wc + e * (G::ES / 4)).x[0];
+                        enc<T, 1>(o, wo + e * (G::ES / 4));
+                    }
+                    sts_group<G::GB>(sY, t, g, wo);
+                }
+                Xr.x[0] = gsuf[0] + gs[0];
+            } else {
 #pragma unroll
             for (int g = G::NG - 1; g >= 0; --g) {
                 uint32_t wa[G::GB / 4], wy[G::GB / 4], wc[G::GB / 4], wo[G::GB / 4], wz[G::GB / 4];
@@ -557,6 +594,7 @@ __global__ void __launch_bounds__(NT + 64, (FWD || ACC) ? 2 : 3) scan_sweep(cons
                 }
                 sts_group<G::GB>(sY, t, g, wo);
                 if (YS) sts_group<G::GB>(sA, t, g, wz);
+            }
             }
             if (has_partial) {
                 store_partial_row(sY, t, p.as_bar, p.full_rows, p.tail_bytes);
