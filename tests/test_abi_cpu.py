@@ -162,3 +162,22 @@ def test_extension_entry_points_validate_without_gpu(L):
     sh1 = VjpShard(0, 1, 0, 10)
     assert L.vjp_scan_partial2(3, 2, 10, p16, p16, p16, 1 << 20, sh1, p16, p16, None, 0) == 1  # world 1
     assert L.vjp_reduce(6, 2, 10, None, p16, p16, None, None, p16, 1 << 20, None, 0) == 1    # MAT2 needs as
+
+
+def test_header_is_plain_c_and_links(tmp_path, L):
+    """include/vjp.h is a C (not C++) header and a C program links against
+    libvjp_b200.so through it (no torch types in the boundary)."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    src = tmp_path / "abi.c"
+    src.write_text('#include "vjp.h"\n#include <stdio.h>\n'
+                   'int main(void) { printf("%s\\n", vjp_status_string(VJP_EINVAL));\n'
+                   '  return vjp_scan_workspace_bytes(VJP_ADD, VJP_F64, 0) == (size_t)-1; }\n')
+    libdir = os.path.join(ROOT, "paper_2202_10297_b200", "_lib")
+    exe = tmp_path / "abi"
+    subprocess.check_call(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"), str(src),
+                           "-L", libdir, "-lvjp_b200", "-o", str(exe)])
+    out = subprocess.run([str(exe)], capture_output=True, text=True, env={**os.environ, "LD_LIBRARY_PATH": libdir})
+    assert out.returncode == 0 and out.stdout.startswith("VJP_EINVAL"), (out.returncode, out.stdout, out.stderr)
