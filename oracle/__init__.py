@@ -48,7 +48,7 @@ def lib():
         build()
         L = ctypes.CDLL(_LIB)
         vp, i64, u32, ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint, ctypes.c_int
-        L.oracle_vjp_scan.argtypes = [ci, ci, i64, vp, vp, vp, vp, u32]
+        L.oracle_vjp_scan.argtypes = [ci, ci, i64, vp, vp, vp, vp, vp, u32]
         L.oracle_vjp_reduce.argtypes = [ci, ci, i64, vp, vp, vp, vp, vp, vp, u32]
         L.oracle_vjp_reduce_by_index.argtypes = [ci, ci, ci, i64, i64, vp, vp, vp, vp, vp, vp, vp, u32]
         L.oracle_vjp_scatter.argtypes = [ci, ci, i64, i64, i64, vp, vp, vp, vp, u32]
@@ -85,11 +85,12 @@ def _op(op) -> int:
 
 
 def vjp_scan(op, ys_bar: np.ndarray, as_: np.ndarray | None = None, *, out=None,
-             accumulate: bool = False, want_ys: bool = False):
+             accumulate: bool = False, want_ys: bool = False, want_cond: bool = False):
     """as_bar of ys = scan op as_ with output adjoint ys_bar.
 
     Arrays are flat, element-interleaved (LINREC: d,c; MAT2: 2x2 row-major).
-    Returns as_bar (and ys if want_ys)."""
+    Returns as_bar (and ys if want_ys, and cond if want_cond: f64 per scalar,
+    the sum of |terms| of each adjoint entry, SURVEY 8c reading A22)."""
     o = _op(op)
     ys_bar = np.ascontiguousarray(ys_bar)
     dt = _dt(ys_bar)
@@ -101,11 +102,13 @@ def vjp_scan(op, ys_bar: np.ndarray, as_: np.ndarray | None = None, *, out=None,
         assert as_.size == ys_bar.size
     as_bar = np.zeros_like(ys_bar) if out is None else out
     ys = np.empty_like(ys_bar) if (want_ys and as_ is not None) else None
-    rc = lib().oracle_vjp_scan(o, dt, n, _p(as_), _p(ys_bar), _p(as_bar), _p(ys),
+    cond = np.zeros(ys_bar.size, dtype=np.float64) if want_cond else None
+    rc = lib().oracle_vjp_scan(o, dt, n, _p(as_), _p(ys_bar), _p(as_bar), _p(ys), _p(cond),
                                ACCUMULATE if accumulate else 0)
     if rc != 0:
         raise RuntimeError(f"oracle_vjp_scan rc={rc}")
-    return (as_bar, ys) if want_ys else as_bar
+    res = (as_bar,) + ((ys,) if want_ys else ()) + ((cond,) if want_cond else ())
+    return res if len(res) > 1 else as_bar
 
 
 def vjp_reduce(op, as_: np.ndarray, y_bar, *, out=None, accumulate: bool = False):

@@ -183,9 +183,23 @@ static void op_vjp(int op, const LD *r, const LD *a, const LD *vbar, LD *ga, LD 
  *     asbar[0] += rbar[0]
  * `as` may be NULL for ADD (the derivative does not read it).  ys (nullable)
  * receives the primal scan.
+ *
+ * cond (nullable, n*W doubles): the condition scale of each adjoint entry,
+ * sum_terms |term| (SURVEY 8c reading A22), for comparing signed data where
+ * an adjoint entry is a cancelling sum.  Every adjoint entry of the loop above
+ * is a sum of products of entries of ysbar, as and rs; cond runs the SAME loop
+ * on |ysbar|, |as| and rs recomputed from |as|, so each product becomes its
+ * absolute value and the sum becomes sum |term| exactly (up to rounding: all
+ * addends are >= 0).  ADD, MUL, LINREC and MAT2 are polynomials with +1
+ * coefficients in these entries (op_apply / op_vjp above), so this is the
+ * literal sum of |monomials|.  MIN / MAX select by comparing the REAL rs and
+ * as (the branch taken is part of the derivative, not a term), so their
+ * selections use the real values and only ysbar is replaced by |ysbar|.
  */
+static void scan_cond(int op, int dtype, int64_t n, const void *as, const void *ys_bar, double *cond);
+
 int oracle_vjp_scan(int op, int dtype, int64_t n, const void *as, const void *ys_bar,
-                    void *as_bar, void *ys, unsigned flags) {
+                    void *as_bar, void *ys, double *cond, unsigned flags) {
     int w = width_of(op);
     if (w == 0 || (dtype != O_F32 && dtype != O_F64) || n < 0) return O_EINVAL;
     if (n == 0) return O_OK;
@@ -222,7 +236,45 @@ int oracle_vjp_scan(int op, int dtype, int64_t n, const void *as, const void *ys
 
     free(rbar);
     free(rs);
+    if (cond) scan_cond(op, dtype, n, as, ys_bar, cond);
     return O_OK;
+}
+
+/* the loop of oracle_vjp_scan on absolute values (see its comment) */
+static void scan_cond(int op, int dtype, int64_t n, const void *as, const void *ys_bar, double *cond) {
+    const int w = width_of(op);
+    const int sel = (op == O_MIN || op == O_MAX);
+    LD *rs = NULL;
+    if (as) {
+        rs = (LD *)malloc(sizeof(LD) * (size_t)n * w);
+        if (!rs) return;
+        for (int k = 0; k < w; ++k) rs[k] = sel ? ld_get(dtype, as, k) : fabsl(ld_get(dtype, as, k));
+        for (int64_t i = 1; i < n; ++i) {
+            LD a[4];
+            for (int k = 0; k < w; ++k) {
+                a[k] = ld_get(dtype, as, i * w + k);
+                if (!sel) a[k] = fabsl(a[k]);
+            }
+            op_apply(op, &rs[(i - 1) * w], a, &rs[i * w]);
+        }
+    }
+    LD *rbar = (LD *)malloc(sizeof(LD) * (size_t)n * w);
+    if (!rbar) { free(rs); return; }
+    for (int64_t i = 0; i < n * w; ++i) rbar[i] = fabsl(ld_get(dtype, ys_bar, i));
+    LD zero[4] = {0, 0, 0, 0};
+    for (int64_t i = n - 1; i >= 1; --i) {
+        LD a[4], ga[4];
+        const LD *r = rs ? &rs[(i - 1) * w] : zero;
+        for (int k = 0; k < w; ++k) {
+            a[k] = as ? ld_get(dtype, as, i * w + k) : 0.0L;
+            if (!sel) a[k] = fabsl(a[k]);
+        }
+        op_vjp(op, r, a, &rbar[i * w], ga, &rbar[(i - 1) * w]);
+        for (int k = 0; k < w; ++k) cond[i * w + k] = (double)ga[k];
+    }
+    for (int k = 0; k < w; ++k) cond[k] = (double)rbar[k];
+    free(rbar);
+    free(rs);
 }
 
 /*

@@ -417,3 +417,53 @@ def test_reduce_general_rule_exact_central_fd(op):
         exp.append((fu - fd) / 2)
     ab, _, _, _ = oracle.vjp_reduce(op, np.array([float(x) for x in a]), np.array([float(x) for x in ybar]))
     assert ab.tolist() == [float(x) for x in exp]
+
+
+# ------------------------------------------- condition scale (reading A22)
+
+@pytest.mark.parametrize("op", ["add", "mul", "linrec", "mat2"])
+@pytest.mark.parametrize("n", [1, 2, 5, 11])
+def test_scan_cond_is_sum_of_abs_terms(op, n):
+    """cond = sum |term| of each adjoint entry.  ADD / MUL / LINREC / MAT2 scans
+    are polynomials with +1 coefficients in (as, ysbar), so sum |monomial| =
+    J(|x|)^T |ybar| — computed here from the exact rational PRIMAL definition
+    by dual numbers (_exact.py), not by the oracle's loop."""
+    rng = random.Random(4242 + 17 * n + len(op))
+    w = OPS[op][1]
+    x = [Fr(rng.randint(-9, 9), 4) for _ in range(n * w)]
+    yb = [Fr(rng.randint(-9, 9), 2) for _ in range(n * w)]
+    exp = vjp_by_duals(lambda v: scan(op, v), [abs(v) for v in x], [abs(v) for v in yb])
+    _, cond = oracle.vjp_scan(op, np.array([float(v) for v in yb]), np.array([float(v) for v in x]),
+                              want_cond=True)
+    assert [Fr(float(c)) for c in cond] == exp  # small dyadic rationals: exact
+
+
+@pytest.mark.parametrize("op", ["min", "max"])
+def test_scan_cond_min_max_selection_from_real_values(op):
+    """MIN / MAX: every adjoint entry is a sum of selected ybar entries (the
+    Jacobian is 0/1 at the REAL inputs), so cond = J(x)^T |ybar| with J from
+    the exact primal definition at x itself."""
+    rng = random.Random(99)
+    n = 12
+    x = [Fr(rng.randint(-3, 3)) for _ in range(n)]
+    yb = [Fr(rng.randint(-7, 7)) for _ in range(n)]
+    exp = vjp_by_duals(lambda v: scan(op, v), x, [abs(v) for v in yb])
+    _, cond = oracle.vjp_scan(op, np.array([float(v) for v in yb]), np.array([float(v) for v in x]),
+                              want_cond=True)
+    assert [Fr(float(c)) for c in cond] == exp
+
+
+def test_scan_cond_add_closed_form_and_bound():
+    """scan(+): cond_i = sum_{j >= i} |ybar_j| (the reversed suffix sum of
+    |ybar|), and |as_bar_i| <= cond_i for signed seeds."""
+    rng = np.random.default_rng(5)
+    yb = rng.integers(-8, 9, size=1000).astype(np.float64)
+    ab, cond = oracle.vjp_scan("add", yb, None, want_cond=True)
+    assert np.array_equal(cond, np.cumsum(np.abs(yb)[::-1])[::-1])
+    assert np.all(np.abs(ab) <= cond)
+    # LINREC with signed data: the adjoint never exceeds its condition scale
+    a = rng.uniform(-1, 1, size=2000)
+    y = rng.uniform(-1, 1, size=2000)
+    ab, cond = oracle.vjp_scan("linrec", y, a, want_cond=True)
+    assert np.all(np.abs(ab) <= cond * (1 + 1e-15))
+    assert cond.min() > 0
