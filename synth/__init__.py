@@ -105,13 +105,45 @@ def mat2_inputs(n, *, dtype=torch.float64, offset=0, device="cpu"):
     return as_, ybar
 
 
-def mul_inputs(n, *, zeros="none", dtype=torch.float32, offset=0, device="cpu", n_total=None):
+def linrec_signed_inputs(n, *, dtype=torch.float64, offset=0, device="cpu"):
+    """signed LINREC (SURVEY 8c A22 comparator): d ~ U(-1,1), c = +-U(0.5, 1)
+    (random sign: |c| < 1 keeps the recurrence contractive while the terms of
+    every adjoint entry cancel), seeds ~ U(-1,1)^2."""
+    d = uniform(n, 220, lo=-1.0, hi=1.0, dtype=torch.float64, offset=offset, device=device)
+    c = uniform(n, 221, lo=0.5, hi=1.0, dtype=torch.float64, offset=offset, device=device)
+    c = torch.where((bits(n, 222, offset=offset, device=device) & 1) == 1, -c, c)
+    as_ = torch.stack([d, c], 1).reshape(-1).to(dtype)
+    ybar = uniform(2 * n, 223, lo=-1.0, hi=1.0, dtype=dtype, offset=2 * offset, device=device)
+    return as_, ybar
+
+
+def mat2_orthogonal_inputs(n, *, dtype=torch.float64, offset=0, device="cpu"):
+    """signed MAT2: rotations / reflections [[p, -s q], [q, s p]] with
+    p = (1 - t^2)/(1 + t^2), q = 2t/(1 + t^2) (the rational parametrisation of
+    the unit circle, no transcendental functions), t ~ U(-1, 1), s = +-1.
+    Every prefix product stays (numerically) orthogonal, so rs neither grows
+    nor decays, while entries of both signs make the adjoint sums cancel;
+    seeds ~ U(-1,1)^4."""
+    t = uniform(n, 230, lo=-1.0, hi=1.0, dtype=torch.float64, offset=offset, device=device)
+    s = torch.where((bits(n, 231, offset=offset, device=device) & 1) == 1, -1.0, 1.0).to(torch.float64)
+    den = 1.0 + t * t
+    p = (1.0 - t * t) / den
+    q = (2.0 * t) / den
+    as_ = torch.stack([p, -s * q, q, s * p], 1).reshape(-1).to(dtype)
+    ybar = uniform(4 * n, 232, lo=-1.0, hi=1.0, dtype=dtype, offset=4 * offset, device=device)
+    return as_, ybar
+
+
+def mul_inputs(n, *, zeros="none", dtype=torch.float32, offset=0, device="cpu", n_total=None, signs=None):
     """config 3 reduce(*): a_i = 1 + (u - 1/2) * 2^-11 (log-centred: the product
     of 2^30 of them stays within ~e^-11..e^11 in f32 and f64).  Zero injection
     (positions from the integer generator, independent of sharding):
       'none' z = 0; 'one' z = 1; 'two' z = 2; 'sparse' each element zero with
       probability 2^-20 (~1024 zeros at 2^30).  The first injected zero of
-      'one'/'two' is -0.0 (must count as a zero, IEEE)."""
+      'one'/'two' is -0.0 (must count as a zero, IEEE).
+    signs: None (all positive), 'random' (each factor negative with
+    probability 1/2), 'odd' / 'even' (random, then the count of negative
+    nonzero factors forced odd / even) — the sign-parity path of P:1040-1061."""
     N = n_total if n_total is not None else n + offset
     u = uniform(n, 300, dtype=torch.float64, offset=offset, device=device)
     a = (1.0 + (u - 0.5) * (2.0 ** -11)).to(dtype)
@@ -125,6 +157,25 @@ def mul_inputs(n, *, zeros="none", dtype=torch.float32, offset=0, device="cpu", 
     elif zeros == "sparse":
         b = bits(n, 302, offset=offset, device=device)
         a[_srl(b, 44) == 0] = 0.0
+    if signs is not None:
+        a = _apply_signs(a, 303, signs, offset)
+    return a
+
+
+def _apply_signs(a, stream, signs, offset):
+    """random signs (bit 0 of stream `stream`), then 'odd' / 'even' fixes the
+    parity of the number of NEGATIVE NONZERO factors by flipping the first
+    nonzero element (whole arrays only, offset 0); 'random' keeps it."""
+    neg = (bits(a.numel(), stream, offset=offset, device=a.device) & 1) == 1
+    a = torch.where(neg, -a, a)
+    if signs in ("odd", "even"):
+        assert offset == 0, "parity control needs the whole array"
+        nz = a != 0
+        cnt = int(((a < 0) & nz).sum())
+        want = 1 if signs == "odd" else 0
+        if cnt % 2 != want and bool(nz.any()):
+            j = int(torch.nonzero(nz)[0])
+            a[j] = -a[j]
     return a
 
 
@@ -143,29 +194,110 @@ def min_inputs(n, *, dtype=torch.float32, offset=0, device="cpu", n_total=None):
 
 
 def rbi_inputs(n, m, op, *, dtype=torch.float64, itype=torch.int32, offset=0, device="cpu",
-               skew=False):
+               skew=False, kind="default"):
     """config 4 reduce_by_index, k-means shaped: bins i.i.d. uniform over m
     (skew=True: bin = floor(m * u^2), a heavy head of small bins); h̄s ~ U(0.5, 1.5).
     '+'/'max'/'min': values on a 2^-12 grid of U(0,1) so per-bin ties at the
     extremum occur (lowest index must win).  '*': log-centred 1 + (u-1/2)2^-10
-    with zeros of probability ~ m/n (per-bin zero count ~ Poisson(1))."""
+    with zeros of probability ~ m/n (per-bin zero count ~ Poisson(1)).
+    kind='wide' (mul): signed factors over 14 binades, log-centred per bin
+    (_rbi_wide_factors); kind='signed' (min/max): negative values, +-0.0 ties
+    and +-inf (_rbi_signed_extrema)."""
     if skew:
         u = uniform(n, 400, offset=offset, device=device)
         inds = torch.clamp((u * u * m).floor(), max=m - 1).to(itype)
     else:
         inds = integers(n, 400, 0, m - 1, offset=offset, device=device, dtype=itype)
-    if op == "mul":
+    if op == "mul" and kind == "wide":
+        a = _rbi_wide_factors(inds, m, device).to(dtype)
+        thr = int(min(1.0, m / max(n, 1)) * (1 << 62))
+        b = _srl(bits(n, 402, offset=offset, device=device), 2)
+        a[b < thr] = 0.0
+    elif op == "mul":
         u = uniform(n, 401, offset=offset, device=device)
         a = (1.0 + (u - 0.5) * (2.0 ** -10)).to(dtype)
         # zero with probability m/n: compare 62 random bits against m/n * 2^62
         thr = int(min(1.0, m / max(n, 1)) * (1 << 62))
         b = _srl(bits(n, 402, offset=offset, device=device), 2)
         a[b < thr] = 0.0
+    elif kind == "signed":
+        a = _rbi_signed_extrema(inds, m, op, offset, device).to(dtype)
     else:
         k = integers(n, 403, 0, (1 << 12) - 1, offset=offset, device=device)
         a = (k.to(torch.float64) * (2.0 ** -12)).to(dtype)
     hs_bar = uniform(m, 404, lo=0.5, hi=1.5, dtype=dtype, device=device)
     return inds, a, hs_bar
+
+
+def _rbi_wide_factors(inds, m, device):
+    """reduce_by_index(*) factors of both signs over 14 binades, log-centred per
+    bin (the verdict's 'a = +-2^g centred per bin', reading R13: every bin's
+    product stays normal in f64 at any bin size):  a_i = s_i * m_i * 2^k_i with
+    m_i ~ U[1, 2), s_i = +-1, and k_i chosen so that, along each bin in index
+    order, the running sum of log2|a| telescopes to  T_i - round(T_i) + d_i
+    (T_i = running sum of log2 m, d_i in [-3, 3] uniform):
+        k_i = -(round(T_i) - round(T_prev)) + d_i - d_prev.
+    So |a_i| spans 2^-7 .. 2^7 while every partial product of a bin stays
+    within 2^+-4.  The float log2 only CHOOSES the integer k_i: the values are
+    exact (m_i * 2^k_i), and the oracle gets the same bits."""
+    n = inds.numel()
+    ii = inds.to(torch.int64)
+    u = uniform(n, 410, device=device)
+    mant = 1.0 + u
+    sgn = torch.where((bits(n, 411, device=device) & 1) == 1, -1.0, 1.0).to(torch.float64)
+    d = integers(n, 412, -3, 3, device=device)
+    ok = (ii >= 0) & (ii < m)
+    key = torch.where(ok, ii, torch.full_like(ii, m))  # out-of-range bins: one extra segment
+    order = torch.sort(key, stable=True).indices
+    ks = key[order]
+    L = torch.log2(mant)[order]
+    cs = torch.cumsum(L, 0)
+    first = torch.ones(n, dtype=torch.bool, device=device)
+    if n > 1:
+        first[1:] = ks[1:] != ks[:-1]
+    seg = torch.cumsum(first.to(torch.int64), 0) - 1
+    base = (cs - L)[first]
+    T = cs - base[seg]
+    R = torch.round(T).to(torch.int64)
+    ds = d[order]
+    Rprev = torch.zeros_like(R)
+    dprev = torch.zeros_like(ds)
+    if n > 1:
+        Rprev[1:] = R[:-1]
+        dprev[1:] = ds[:-1]
+    Rprev[first] = 0
+    dprev[first] = 0
+    ksh = -(R - Rprev) + ds - dprev
+    k = torch.empty_like(ksh)
+    k[order] = ksh
+    return sgn * torch.ldexp(mant, k.to(torch.float64))
+
+
+def _rbi_signed_extrema(inds, m, op, offset, device):
+    """reduce_by_index(min/max) values with the comparison hazards (reading A9):
+    k * 2^-12 for k uniform in [-4096, 4096] (negative values, exact ties);
+    bins b = 0 mod 5: only values <= 0 (so the extremum sits at 0 for max),
+    each set to +-0.0 with probability 1/16 (IEEE ties of -0.0 and +0.0: the
+    lowest index must win); bins b = 1 mod 7: +inf with probability 1/64,
+    b = 2 mod 7: -inf with probability 1/64 (ties at infinity); bins
+    b = 3 mod 7: every value is the losing infinity (-inf for max, +inf for
+    min), so the extremum IS that infinity and the lowest index wins."""
+    n = inds.numel()
+    ii = inds.to(torch.int64)
+    k = integers(n, 420, -4096, 4096, offset=offset, device=device)
+    a = k.to(torch.float64) * (2.0 ** -12)
+    r = _srl(bits(n, 421, offset=offset, device=device), 40)  # 24 random bits
+    sgn0 = (bits(n, 422, offset=offset, device=device) & 1) == 1
+    b5 = (ii % 5) == 0
+    a = torch.where(b5, -a.abs(), a)
+    z = b5 & (r < (1 << 20))  # 1/16
+    a = torch.where(z, torch.where(sgn0, -0.0, 0.0), a)
+    inf_p = r >= ((1 << 24) - (1 << 18))  # 1/64
+    a = torch.where(((ii % 7) == 1) & inf_p, float("inf"), a)
+    a = torch.where(((ii % 7) == 2) & inf_p, float("-inf"), a)
+    lose = float("-inf") if op == "max" else float("inf")
+    a = torch.where((ii % 7) == 3, lose, a)
+    return a
 
 
 def scatter_inputs(n, m, *, dtype=torch.float64, itype=torch.int64, device="cpu", oob=0):
