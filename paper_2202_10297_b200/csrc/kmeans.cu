@@ -228,6 +228,10 @@ __global__ void __launch_bounds__(KM_NT, 2) km_assign(const T *__restrict__ P, c
             }
         }
         const int64_t gp = p0 + pp;
+        // no candidate compared smaller (NaN coordinates, or every distance
+        // +inf): the first center, as the oracle's strict-compare loop keeps it
+        // (the assignment indexes the per-center tables: never out of range)
+        if (j < 0 || j >= k) j = 0;
         if (gp < n) {
             assign[gp] = j;
             md = fmax(pn[pp] + v, 0.0);
@@ -429,6 +433,7 @@ __global__ void __launch_bounds__(KM_MMA_NT, 2) km_assign_mma(const T *__restric
             v = v1;
             j = j1;
         }
+        if (j < 0 || j >= k) j = 0;  // no candidate compared smaller (see km_assign)
         if (p0 + t < n) {
             assign[p0 + t] = j;
             md = fmax(pn[t] + v, 0.0);

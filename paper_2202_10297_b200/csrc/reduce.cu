@@ -62,6 +62,11 @@ __host__ __device__ __forceinline__ RRec rrec_combine(const RRec &x, const RRec 
 }
 
 template <int OP>
+__global__ void reduce_id_record(RRec *r) {
+    if (threadIdx.x == 0) *r = rrec_id<OP>();
+}
+
+template <int OP>
 __device__ __forceinline__ void rrec_add(RRec &r, double x, int64_t idx) {
     if (OP == VJP_ADD) r.a += x;
     if (OP == VJP_MUL) {
@@ -480,10 +485,22 @@ vjp_status vjp_reduce(vjp_op op, vjp_dtype dtype, int64_t n, const void *as, con
 
 vjp_status vjp_reduce_partial(vjp_op op, vjp_dtype dtype, int64_t n, const void *as, void *ws, size_t ws_bytes,
                               const vjp_shard *shard, void *partial, vjp_stream_t stream) {
-    if (!shard || !partial || n <= 0) return VJP_EINVAL;
+    if (!shard || !partial || n < 0) return VJP_EINVAL;
     vjp_status st = check(op, dtype, n, as, ws, ws_bytes);
     if (st != VJP_OK) return st;
     if (!vjph::aligned16(partial)) return VJP_EALIGN;
+    if (n == 0) {  // empty shard: the neutral record
+        RRec *r = static_cast<RRec *>(partial);
+        cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+        switch (op) {
+        case VJP_ADD: reduce_id_record<VJP_ADD><<<1, 32, 0, s>>>(r); break;
+        case VJP_MUL: reduce_id_record<VJP_MUL><<<1, 32, 0, s>>>(r); break;
+        case VJP_MIN: reduce_id_record<VJP_MIN><<<1, 32, 0, s>>>(r); break;
+        default: reduce_id_record<VJP_MAX><<<1, 32, 0, s>>>(r); break;
+        }
+        vjph::count_launch();
+        return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+    }
     return run_fwd(op, dtype, as, n, shard->global_offset, ws, static_cast<RRec *>(partial),
                    reinterpret_cast<cudaStream_t>(stream));
 }
@@ -491,11 +508,12 @@ vjp_status vjp_reduce_partial(vjp_op op, vjp_dtype dtype, int64_t n, const void 
 vjp_status vjp_reduce_finish(vjp_op op, vjp_dtype dtype, int64_t n, const void *as, const void *y_bar, void *as_bar,
                              void *y, int64_t *arg, void *ws, size_t ws_bytes, const vjp_shard *shard,
                              const void *gathered, vjp_stream_t stream, unsigned flags) {
-    if (!shard || !gathered || n <= 0 || shard->world < 1) return VJP_EINVAL;
+    if (!shard || !gathered || n < 0 || shard->world < 1) return VJP_EINVAL;
     vjp_status st = check(op, dtype, n, as, ws, ws_bytes);
     if (st != VJP_OK) return st;
-    if (!y_bar || !as_bar) return VJP_EINVAL;
-    if (!vjph::aligned16(as_bar)) return VJP_EALIGN;
+    if (!y_bar || (n > 0 && !as_bar)) return VJP_EINVAL;
+    if (n > 0 && !vjph::aligned16(as_bar)) return VJP_EALIGN;
+    if (n == 0 && !y && !arg) return VJP_OK;  // empty shard, no primal outputs requested
     RBwd p{};
     p.n = n;
     p.goff = shard->global_offset;
@@ -503,8 +521,10 @@ vjp_status vjp_reduce_finish(vjp_op op, vjp_dtype dtype, int64_t n, const void *
     p.acc = (flags & VJP_ACCUMULATE) ? 1 : 0;
     p.recs = static_cast<const RRec *>(gathered);
     p.ybar = y_bar;
-    p.y = shard->rank == 0 ? y : nullptr;
-    p.arg = shard->rank == 0 ? arg : nullptr;
+    // every rank combines the same records in the same order: y / arg are
+    // identical everywhere, so every rank writes them
+    p.y = y;
+    p.arg = arg;
     return run_bwd(op, dtype, as, as_bar, p, reinterpret_cast<cudaStream_t>(stream));
 }
 

@@ -119,7 +119,7 @@ def reduce(op, as_: torch.Tensor, y_bar, *, offset: int, global_n: int, group=No
     dt = _dt(as_)
     L = lib()
     sh = _shard(offset, n, global_n, group)
-    yb = y_bar.reshape(1).to(as_.dtype) if isinstance(y_bar, torch.Tensor) else torch.full(
+    yb = y_bar.reshape(1).to(device=dev, dtype=as_.dtype) if isinstance(y_bar, torch.Tensor) else torch.full(
         (1,), float(y_bar), dtype=as_.dtype, device=dev)
     ab = out if out is not None else torch.empty_like(as_)
     y = torch.empty(1, dtype=as_.dtype, device=dev) if want_y else None
