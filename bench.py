@@ -187,6 +187,65 @@ def run_reference(args):
     return 0
 
 
+def measure_targets(args, dev, peak):
+    """The north_star target kernels (BASELINE.json: vjp_scan + and the 2x2
+    linear recurrence at 2^30 f64, vjp_reduce_by_index +/x/max at n = 2^28 with
+    m = 10^3 and 10^6), each timed alone on one GPU: CUDA events around each
+    call on the launching stream, median over `steps` calls after `warmup`,
+    NVML clocks sampled during that target's own timed region.  Method bytes
+    per element: scan(+) 16, LINREC 64 (forward re-execution reads
+    `as` once more), rbi + 12, x 32, max 20.  Inputs >= 2 GiB per array (no L2
+    flush needed); each target's arrays are freed before the next."""
+    import torch
+
+    import paper_2202_10297_b200 as vjp
+    import synth
+
+    steps = max(5, min(args.steps, 10))
+    out = []
+
+    def one(name, workload, n, nbytes, fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        with ClockSampler(dev.index) as clk:
+            for e0, e1 in ev:
+                e0.record()
+                fn()
+                e1.record()
+            torch.cuda.synchronize()
+        ts = [a.elapsed_time(b) for a, b in ev]
+        ms = statistics.median(ts)
+        gbs = nbytes / (ms * 1e-3) / 1e9
+        out.append({"name": name, "workload": workload, "n": n, "ms": ms, "mean_ms": statistics.mean(ts),
+                    "min_ms": min(ts), "steps": steps, "elements_per_s": n / (ms * 1e-3),
+                    "method_bytes": nbytes, "alg_gbs": gbs, "peak_gbs": peak, "frac": gbs / peak,
+                    "clocks": clk.summary()})
+
+    N30, N28 = 1 << 30, 1 << 28
+    yb = synth.scan_add_seed(N30, device=dev)
+    ab = torch.empty_like(yb)
+    one("scan(+) f64 2^30", "vjp_scan ADD, n = 2^30 f64 (config 1 at the target size)", N30, 16 * N30,
+        lambda: vjp.scan("add", yb, out=ab))
+    del yb, ab
+    a, yb = synth.linrec_inputs(N30, device=dev)
+    ab = torch.empty_like(yb)
+    one("LINREC f64 2^30", "vjp_scan LINREC, n = 2^30 f64", N30, 64 * N30,
+        lambda: vjp.scan("linrec", yb, a, out=ab))
+    del a, yb, ab
+    for m in (1000, 1_000_000):
+        for op, nb in (("add", 12), ("mul", 32), ("max", 20)):
+            inds, a, hb = synth.rbi_inputs(N28, m, op, device=dev)
+            o = torch.empty(N28, dtype=torch.float64, device=dev)
+            one(f"rbi {op} m={m}", f"vjp_reduce_by_index {op.upper()}, n = 2^28 f64, int32 bins, m = {m} "
+                "(config 4, uniform bins)", N28, nb * N28,
+                lambda op=op, inds=inds, a=a, hb=hb, o=o: vjp.reduce_by_index(op, inds, a, hb, out=o))
+            del inds, a, hb, o
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -332,6 +391,11 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
+        if world == 1 and not args.no_targets:
+            for op in ops:  # free the headline arrays first
+                data[op] = None
+            torch.cuda.empty_cache()
+            line["targets"] = measure_targets(args, dev, peak)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -490,6 +554,7 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="override elements per op per GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-targets", action="store_true", help="skip the north_star target kernels (1 GPU)")
     ap.add_argument("--workload", default="config2",
                     choices=["config2", "scan_add", "scan_linrec30", "reduce", "rbi", "kmeans", "batched", "all"],
                     help="config2 = the headline line; the others print per-call extra lines")

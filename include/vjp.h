@@ -96,7 +96,10 @@ enum {
                                     kernel, as/ys_bar read from HBM once, each round re-read
                                     from L2) for any of ADD/MUL/LINREC/MAT2; it is already the
                                     default for f64 ADD without ys */
-    VJP_SCAN_CHUNKED = 1u << 18   /* tuning/testing: force the two chunked kernels */
+    VJP_SCAN_CHUNKED = 1u << 18,  /* tuning/testing: force the two chunked kernels */
+    VJP_SCAN_BLOCKLB = 1u << 19   /* tuning/testing: force the one-read block look-back
+                                    (single GPU; the default for every operator except f64
+                                    scan(+) without ys) */
 };
 
 /* One shard of a multi-GPU call: this process owns global elements

@@ -30,6 +30,7 @@ CHECK_INDICES = 2
 SCAN_LOOKBACK = 1 << 16
 SCAN_SWEEP = 1 << 17
 SCAN_CHUNKED = 1 << 18
+SCAN_BLOCKLB = 1 << 19
 STATUS = {0: "VJP_OK", 1: "VJP_EINVAL", 2: "VJP_EUNSUPPORTED", 3: "VJP_EWORKSPACE", 4: "VJP_ECUDA",
           5: "VJP_EDUPINDEX", 6: "VJP_EOOB", 7: "VJP_EALIGN"}
 
@@ -164,11 +165,28 @@ def _to(t, dev):
     return src.to(dev, non_blocking=True)
 
 
+def _check_out(out, numel: int, dtype, dev, what: str = "out"):
+    """the kernels write numel * sizeof(dtype) bytes through out's data pointer:
+    refuse anything that is not exactly that (size, dtype, device, layout)."""
+    if out.numel() != numel:
+        raise ValueError(f"vjp: {what} has {out.numel()} elements, expected {numel}")
+    if out.dtype != dtype:
+        raise TypeError(f"vjp: {what} is {out.dtype}, expected {dtype}")
+    if out.is_cuda and out.device != torch.device(dev):
+        raise ValueError(f"vjp: {what} is on {out.device}, the call runs on {dev}")
+    if not out.is_contiguous():
+        raise ValueError(f"vjp: {what} must be contiguous")
+
+
 def _out_buf(out, like, dev, accumulate):
     """device buffer for an output: `out` itself if on the device; for a host
-    `out`, a device temporary (pre-loaded only when accumulating)."""
+    `out`, a device temporary (pre-loaded only when accumulating).  With
+    accumulate=True the caller must pass the adjoint to add into."""
     if out is None:
+        if accumulate:
+            raise ValueError("vjp: accumulate=True adds into `out`: pass the existing adjoint")
         return torch.empty_like(like, device=dev)
+    _check_out(out, like.numel(), like.dtype, dev)
     if out.is_cuda:
         return out
     return _to(out, dev) if accumulate else torch.empty(out.shape, dtype=out.dtype, device=dev)
@@ -192,15 +210,17 @@ def _host_out(t: torch.Tensor, like_host: bool):
 # ----------------------------------------------------------------- calls
 
 def scan(op, ys_bar: torch.Tensor, as_: torch.Tensor | None = None, *, out: torch.Tensor | None = None,
-         want_ys: bool = False, accumulate: bool = False, lookback: bool = False, sweep: bool = False, chunked: bool = False):
+         want_ys: bool = False, accumulate: bool = False, lookback: bool = False, sweep: bool = False, chunked: bool = False,
+         blocklb: bool = False):
     """as_bar of ``ys = scan op as_`` with output adjoint ``ys_bar`` (sec 5.2).
 
     Tensors hold n elements of the operator's width (LINREC: (d, c) pairs,
     MAT2: row-major 2x2), any shape with that many scalars.  Returns as_bar
     (same shape as ys_bar), or (as_bar, ys) if want_ys.  lookback=True selects
     the single-sweep decoupled look-back kernels, sweep=True the one-read
-    L2-round sweep, chunked=True the two chunked kernels (tuning/testing; the
-    default is the sweep for scan(+) and the chunked kernels otherwise)."""
+    L2-round sweep, chunked=True the two chunked kernels, blocklb=True the
+    one-read block look-back (tuning/testing; the default on one GPU is the
+    block look-back, and the L2-round sweep for f64 scan(+) without ys)."""
     o = _op(op)
     host = not ys_bar.is_cuda
     dev = _dev_of(ys_bar, as_, out)
@@ -219,7 +239,8 @@ def scan(op, ys_bar: torch.Tensor, as_: torch.Tensor | None = None, *, out: torc
     _check(L.vjp_scan(o, _dt(yb), n, _p(a), _p(yb), _p(ab), _p(ys), _p(ws),
                       0 if ws is None else ws.numel(), _stream(dev),
                       (ACCUMULATE if accumulate else 0) | (SCAN_LOOKBACK if lookback else 0)
-                      | (SCAN_SWEEP if sweep else 0) | (SCAN_CHUNKED if chunked else 0)),
+                      | (SCAN_SWEEP if sweep else 0) | (SCAN_CHUNKED if chunked else 0)
+                      | (SCAN_BLOCKLB if blocklb else 0)),
            "vjp_scan")
     if out is not None and not out.is_cuda:
         out.copy_(ab, non_blocking=True)
@@ -334,6 +355,10 @@ def scatter(is_: torch.Tensor, ys_bar: torch.Tensor, *, width: int = 1, in_place
         raise ValueError("in_place scatter needs device tensors")
     n, m = yb.numel() // width, ix.numel()
     xb = yb if in_place else torch.empty_like(yb)
+    if vs_out is not None:
+        _check_out(vs_out, m * width, yb.dtype, dev, "vs_out")
+    elif accumulate:
+        raise ValueError("vjp: accumulate=True adds into `vs_out`: pass the existing adjoint")
     vb = _to(vs_out, dev) if vs_out is not None else torch.empty(m * width, dtype=yb.dtype, device=dev)
     flags = (ACCUMULATE if accumulate else 0) | (CHECK_INDICES if check else 0)
     L = lib()
@@ -355,6 +380,8 @@ def scatter_forward(xs: torch.Tensor, is_: torch.Tensor, vs: torch.Tensor, *, wi
     n, m = xs.numel() // width, ix.numel()
     if v.numel() != m * width or v.dtype != xs.dtype:
         raise ValueError("vs must be [m x width] of xs's dtype")
+    if saved_out is not None:
+        _check_out(saved_out, m * width, xs.dtype, dev, "saved_out")
     saved = saved_out if saved_out is not None else torch.empty(m * width, dtype=xs.dtype, device=dev)
     L = lib()
     ws = workspace(L.vjp_scatter_workspace_bytes(_dt(xs), n, m), dev) if check else None

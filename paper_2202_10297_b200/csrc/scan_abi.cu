@@ -110,6 +110,13 @@ vjp_status reduce_general(vjp_op op, vjp_dtype dtype, int64_t n, const void *as,
 }
 }  // namespace vjph
 
+namespace vjph {
+unsigned long long *&lb_trace_ptr() {
+    static unsigned long long *p = nullptr;
+    return p;
+}
+}  // namespace vjph
+
 extern "C" {
 
 size_t vjp_scan_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_t n) {
@@ -156,9 +163,10 @@ vjp_status vjp_scan_partial(vjp_op op, vjp_dtype dtype, int64_t n, const void *a
     if (s != VJP_OK) return s;
     if (partial && !aligned16(partial)) return VJP_EALIGN;
     if (n == 0) {
-        // empty shard: identity record (neutral forward element, identity map)
+        // empty shard (global_n < world, or an uneven split): identity record
+        // (neutral forward element, identity map); nothing else to do
         if (!partial) return VJP_OK;
-        return VJP_EUNSUPPORTED;  // empty shards are not supported in the split API
+        return disp_for(op)(kScanIdentity, c, nullptr);
     }
     return disp_for(op)(kScanPartial, c, nullptr);
 }
@@ -173,8 +181,8 @@ vjp_status vjp_scan_partial2(vjp_op op, vjp_dtype dtype, int64_t n, const void *
     c.gathered = gathered1;
     vjp_status s = check(c, false);
     if (s != VJP_OK) return s;
-    if (n == 0) return VJP_EUNSUPPORTED;
     if (!partial2 || !aligned16(partial2) || !gathered1 || !aligned16(gathered1)) return VJP_EINVAL;
+    if (n == 0) return disp_for(op)(kScanIdentity, c, nullptr);  // empty shard: identity record
     return disp_for(op)(kScanPartial2, c, nullptr);
 }
 
@@ -206,6 +214,13 @@ vjp_status vjp_scan_carries_host(vjp_op op, vjp_dtype dtype, int32_t rank, int32
     case VJP_MAX: carries_host<vjpk::OpMax>(g, rank, world, fwd_carry, rev_carry); return VJP_OK;
     }
     return VJP_EINVAL;
+}
+
+// tuning hook: per-block timestamps of the block look-back (DEVICE buffer of
+// 8 u64 per block, zeroed by the caller; nullptr turns it off)
+vjp_status vjp_debug_lb_trace(unsigned long long *buf) {
+    vjph::lb_trace_ptr() = buf;
+    return VJP_OK;
 }
 
 }  // extern "C"

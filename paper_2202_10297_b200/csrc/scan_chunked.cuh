@@ -766,6 +766,19 @@ __global__ void __launch_bounds__(NT, 1) scan_apply(const __grid_constant__ CUte
     if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// the record of an EMPTY shard (multi-GPU split with n_local = 0): the neutral
+// forward element and the identity reverse map, so the carry combination of
+// the other ranks passes straight through it
+template <class Op>
+__global__ void scan_identity_record(double *rec) {
+    if (threadIdx.x == 0) {
+        const typename Op::Val e = Op::fwd_id();
+#pragma unroll
+        for (int q = 0; q < Op::W; ++q) rec[q] = e.x[q];
+        map_to<Op>(Op::map_id(), rec + Op::W);
+    }
+}
+
 // ordered combination of the chunk records' forward parts (the primal
 // reduction of the general reduce rule), one CTA
 template <class Op, class T, int NT>

@@ -8,9 +8,33 @@
 #include <cstdio>
 #include <cstdlib>
 
-#include "scan_sweep.cuh"
+#include "scan_blocklb.cuh"
 
 namespace vjph {
+
+// Tuning knobs of the scan paths, read ONCE per process (first use) from the
+// environment — never per call, so a call's behaviour depends only on its
+// arguments and on these process-wide constants (documented in vjp.h):
+//   VJP_LB_L2_MB      block look-back: L2 bytes held by the blocks in flight (MB)
+//   VJP_LB_VARIANT    block look-back TMA stages (0: 3, 1: 2)
+//   VJP_SWEEP_K / VJP_SWEEP_D / VJP_SWEEP_ROUND_MB   one-read sweep geometry
+struct ScanTune {
+    int lb_l2_mb, lb_variant, sweep_k, sweep_d, sweep_round_mb;
+};
+inline int tune_env(const char *name, int dflt) {
+    const char *v = std::getenv(name);
+    return (v && *v) ? std::atoi(v) : dflt;
+}
+inline const ScanTune &scan_tune() {
+    static const ScanTune t{tune_env("VJP_LB_L2_MB", 40), tune_env("VJP_LB_VARIANT", 0), tune_env("VJP_SWEEP_K", 0),
+                            tune_env("VJP_SWEEP_D", 1),
+                            tune_env("VJP_SWEEP_ROUND_MB", 32)};
+    return t;
+}
+
+// tuning only: a device buffer for per-block timestamps of the block look-back
+// (set by vjp_debug_lb_trace; nullptr = off)
+unsigned long long *&lb_trace_ptr();
 
 struct ScanCall {
     vjp_op op;
@@ -31,7 +55,7 @@ struct ScanCall {
 };
 
 enum ScanPhase { kScanWs = 0, kScanPartial = 1, kScanFinish = 2, kScanPartialBytes = 3, kReduceGeneral = 4,
-                 kScanPartial2 = 5 };
+                 kScanPartial2 = 5, kScanIdentity = 6 };
 
 template <class Op, class T>
 struct ScanImpl {
@@ -50,7 +74,8 @@ struct ScanImpl {
         int64_t ntiles;
         size_t counters, flags1, flags2, memset_bytes, p1agg, p1inc, p2agg, p2inc, partial;
         int64_t ntiles_c;
-        size_t tileF, tileP, chunkRec, counter_c, roundRec, arrive, total;
+        size_t tileF, tileP, chunkRec, counter_c, roundRec, arrive, lbFlags, lbAgg, lbInc, lbTileF, lbTileP, lbPark,
+            total;
     };
     static Layout layout(int64_t n) {
         Layout L{};
@@ -73,6 +98,15 @@ struct ScanImpl {
         // sweep: R*G <= ntiles_c/K + G <= ntiles_c + kMaxChunks records; R <= ntiles_c
         L.roundRec = off; off += align256((size_t)(L.ntiles_c + kMaxChunks) * MD * 8);
         L.arrive = off; off += align256((size_t)(L.ntiles_c + 1) * 4);
+        // block look-back: [ticket | pad to 256 B | flags per block], maps and
+        // inclusive values per block (at most one block per tile)
+        const int64_t ntl = ntiles_of(n, NTL_MIN);
+        L.lbFlags = off; off += 256 + align256((size_t)ntl * 4);
+        L.lbAgg = off; off += align256((size_t)ntl * MD * 8);
+        L.lbInc = off; off += align256((size_t)ntl * W * 8);
+        L.lbTileF = off; off += align256((size_t)ntl * W * 8);
+        L.lbTileP = off; off += align256((size_t)ntl * W * 8);
+        L.lbPark = off; off += align256((size_t)NTL_MIN * (W + MD) * 8);  // the last tile's parked rows
         L.total = off;
         return L;
     }
@@ -290,10 +324,10 @@ struct ScanImpl {
     // take it only on request (their shuffle scans of d-vector maps make it
     // slower than the chunked kernels)
     static bool use_sweep(const ScanCall &c) {
-        if (c.world != 1 || (c.flags & (VJP_SCAN_LOOKBACK | VJP_SCAN_CHUNKED))) return false;
+        if (c.world != 1 || (c.flags & (VJP_SCAN_LOOKBACK | VJP_SCAN_CHUNKED | VJP_SCAN_BLOCKLB))) return false;
+        if (c.ys) return false;  // the sweep does not write the primal ys (the other paths do)
         if (c.flags & VJP_SCAN_SWEEP) return true;
-        return std::is_same<Op, vjpk::OpAdd>::value && sizeof(T) == 8 && c.ys == nullptr &&
-               env_int("VJP_SCAN_NO_SWEEP", 0) == 0;
+        return std::is_same<Op, vjpk::OpAdd>::value && sizeof(T) == 8 && c.ys == nullptr;
     }
 
     template <bool FWD, bool ACC, bool YS>
@@ -329,11 +363,6 @@ struct ScanImpl {
         return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
     }
 
-    static int env_int(const char *name, int dflt) {
-        const char *v = std::getenv(name);
-        return (v && *v) ? std::atoi(v) : dflt;
-    }
-
     template <bool FWD, bool ACC, bool YS>
     static vjp_status launch_sweep(const ScanCall &c, const Layout &L) {
         constexpr int S = sw_stages<FWD, ACC, YS>();
@@ -349,10 +378,10 @@ struct ScanImpl {
         int64_t G = (int64_t)sm_count() * occ;
         if (G > kMaxChunks) G = kMaxChunks;
         // tiles per CTA per round: about `round_mb` MB of HBM-read input per round
-        const int64_t round_bytes = (int64_t)env_int("VJP_SWEEP_ROUND_MB", 32) << 20;
+        const int64_t round_bytes = (int64_t)scan_tune().sweep_round_mb << 20;
         int64_t K = round_bytes / (G * NBR * NTC * vjpk::kRowBytes);
         if (std::is_same<Op, vjpk::OpAdd>::value) K = 4;  // measured best for scan(+) at 2^26..2^30 (DESIGN 7.6)
-        K = env_int("VJP_SWEEP_K", (int)K);
+        if (scan_tune().sweep_k > 0) K = scan_tune().sweep_k;
         if (K < 1) K = 1;
         if (K > vjpk::kSweepKMax) K = vjpk::kSweepKMax;
         if (G * K > L.ntiles_c) {  // small inputs: fewer, fuller CTAs
@@ -362,7 +391,7 @@ struct ScanImpl {
         sp.G = (int32_t)G;
         sp.K = (int32_t)K;
         sp.R = (int32_t)((L.ntiles_c + G * K - 1) / (G * K));
-        sp.D = env_int("VJP_SWEEP_D", 1) >= 2 ? 2 : 1;
+        sp.D = scan_tune().sweep_d >= 2 ? 2 : 1;
         unsigned char *ws = static_cast<unsigned char *>(c.ws);
         sp.roundRec = reinterpret_cast<double *>(ws + L.roundRec);
         sp.arrive = reinterpret_cast<uint32_t *>(ws + L.arrive);
@@ -372,9 +401,6 @@ struct ScanImpl {
         const bool f64 = sizeof(T) == 8;
         if (!make_row_tmap(&mab32, c.as_bar, sp.c.full_rows, f64, 32)) return VJP_ECUDA;
         if (!make_row_tmap(&mys32, c.ys, c.ys ? sp.c.full_rows : 0, f64, 32)) return VJP_ECUDA;
-        if (env_int("VJP_SWEEP_DEBUG", 0))
-            fprintf(stderr, "vjp sweep: occ=%d G=%d K=%d R=%d D=%d smem=%zu ntiles=%lld\n", occ, sp.G, sp.K, sp.R, sp.D, sm,
-                    (long long)L.ntiles_c);
         void *args[] = {&ma, &my, &mab, &mab32, &mys32, &sp};
         cudaError_t e = cudaLaunchCooperativeKernel((const void *)k, dim3((unsigned)G), dim3(NTH), args, sm, c.stream);
         if (e == cudaErrorCooperativeLaunchTooLarge) {
@@ -411,6 +437,116 @@ struct ScanImpl {
             return s2 == VJP_OK ? finish_c(c) : s2;
         }
         return st;
+    }
+
+    // ---------------- one-read block look-back (world == 1; scan_blocklb.cuh) ----------------
+    static bool use_lb(const ScanCall &c) {
+        if (c.world != 1 || (c.flags & VJP_ACCUMULATE)) return false;  // ACCUMULATE: as_bar holds inputs
+        if (c.flags & VJP_SCAN_BLOCKLB) return true;
+        if (c.flags & (VJP_SCAN_LOOKBACK | VJP_SCAN_CHUNKED | VJP_SCAN_SWEEP)) return false;
+        return false;  // opt-in until measured faster (DESIGN 7.1c)
+    }
+    // geometry of the block look-back: NTL = 128 rows (one per compute thread)
+    // per tile, SL TMA stages; the forward pre-pass (K_F + tile prefix) runs on
+    // the same tiles.  Variants (scan_tune().lb_variant): 0 = 3 stages, 1 = 2.
+    static constexpr int NTL_MIN = 128;
+    static int64_t ntiles_of(int64_t n, int nt) { return n > 0 ? (n + (int64_t)G::EPR * nt - 1) / ((int64_t)G::EPR * nt) : 0; }
+    template <int NTL>
+    static vjpk::ChunkParams lb_cparams(const ScanCall &c, const Layout &L, int nchunks) {
+        vjpk::ChunkParams p = cparams(c, L, nchunks);
+        p.ntiles = (int32_t)ntiles_of(c.n, NTL);
+        unsigned char *ws = static_cast<unsigned char *>(c.ws);
+        p.tileF = reinterpret_cast<double *>(ws + L.lbTileF);
+        p.tileP = reinterpret_cast<double *>(ws + L.lbTileP);
+        return p;
+    }
+    template <int NTL>
+    static bool lb_maps(const ScanCall &c, int64_t rows, CUtensorMap *m_as, CUtensorMap *m_yb, CUtensorMap *m_ab,
+                        CUtensorMap *m_ys) {
+        const bool f64 = sizeof(T) == 8;
+        bool ok = true;
+        ok &= make_row_tmap(m_as, c.as, c.as ? rows : 0, f64, NTL);
+        ok &= make_row_tmap(m_yb, c.ys_bar, rows, f64, NTL);
+        ok &= make_row_tmap(m_ab, c.as_bar, c.as_bar ? rows : 0, f64, NTL);
+        ok &= make_row_tmap(m_ys, c.ys, c.ys ? rows : 0, f64, NTL);
+        return ok;
+    }
+    // K_F on NTL-row tiles: forward tile aggregates (tileF) + per-chunk records
+    template <int NTL>
+    static vjp_status lb_forward(const ScanCall &c, const Layout &L) {
+        auto k = vjpk::scan_reduce<Op, T, NTL, SC, true, false>;
+        const size_t sm = 1024 + (size_t)SC * NTL * vjpk::kRowBytes + sizeof(vjpk::ReduceSmem<Op, NTL, SC>);
+        int occ = 0;
+        set_smem(k, sm);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NTL, sm) != cudaSuccess || occ < 1) occ = 1;
+        int64_t g = (int64_t)sm_count() * occ;
+        const int64_t nt = ntiles_of(c.n, NTL);
+        if (g > kMaxChunks) g = kMaxChunks;
+        if (g > nt) g = nt;
+        vjpk::ChunkParams p = lb_cparams<NTL>(c, L, (int)(g < 1 ? 1 : g));
+        CUtensorMap ma, my, mab, mys;
+        if (!lb_maps<NTL>(c, p.full_rows, &ma, &my, &mab, &mys)) return VJP_ECUDA;
+        k<<<(unsigned)p.nchunks, NTL, sm, c.stream>>>(ma, my, p);
+        vjpk::scan_tile_prefix<Op, NTL><<<(unsigned)p.nchunks, NTL, 0, c.stream>>>(p);
+        count_launch(2);
+        return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+    }
+    template <int NTL, int SL, bool FWD, bool YS, bool RS>
+    static vjp_status launch_lb(const ScanCall &c, const Layout &L) {
+        auto k = vjpk::scan_blocklb<Op, T, NTL, SL, FWD, YS, RS>;
+        constexpr int NB = (FWD ? 1 : 0) + 1;
+        constexpr int NTH = vjpk::kLbCompute + 32;  // 4 compute warps + the look-back warp
+        const size_t sm = 1024 + (size_t)SL * NB * NTL * vjpk::kRowBytes + sizeof(vjpk::LbSmem<Op, NTL, SL>);
+        set_smem(k, sm);
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NTH, sm) != cudaSuccess || occ < 1) occ = 1;
+        vjpk::LbParams P{};
+        P.c = lb_cparams<NTL>(c, L, 1);
+        const int64_t nt = P.c.ntiles;
+        int64_t G = (int64_t)sm_count() * occ;
+        // tiles per block: the blocks in flight (two per CTA, between their R
+        // and A phases) hold ~2 * G * B * NB tiles in L2
+        int64_t B = ((int64_t)scan_tune().lb_l2_mb << 20) / (2 * G * NB * NTL * vjpk::kRowBytes);
+        if (B < 1) B = 1;
+        if (B > vjpk::kLbBMax) B = vjpk::kLbBMax;
+        if (B * G > nt) {  // small inputs: more, smaller blocks keep every CTA busy
+            B = nt / G;
+            if (B < 1) B = 1;
+        }
+        P.B = (int32_t)B;
+        P.nblocks = (int32_t)((nt + B - 1) / B);
+        unsigned char *ws = static_cast<unsigned char *>(c.ws);
+        P.ticket = reinterpret_cast<uint32_t *>(ws + L.lbFlags);
+        P.flags = reinterpret_cast<uint32_t *>(ws + L.lbFlags + 256);
+        P.agg = reinterpret_cast<double *>(ws + L.lbAgg);
+        P.inc = reinterpret_cast<double *>(ws + L.lbInc);
+        P.tailpark = reinterpret_cast<double *>(ws + L.lbPark);
+        P.trace = lb_trace_ptr();
+        if (cudaMemsetAsync(ws + L.lbFlags, 0, 256 + (size_t)P.nblocks * 4, c.stream) != cudaSuccess) return VJP_ECUDA;
+        CUtensorMap ma, my, mab, mys;
+        if (!lb_maps<NTL>(c, P.c.full_rows, &ma, &my, &mab, &mys)) return VJP_ECUDA;
+        const int64_t grid = G < P.nblocks ? G : P.nblocks;
+        k<<<(unsigned)grid, NTH, sm, c.stream>>>(ma, my, mab, mys, P);
+        count_launch();
+        return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+    }
+    template <int NTL, int SL>
+    static vjp_status run_lb(const ScanCall &c, bool fwd_phase) {
+        Layout L = layout(c.n);
+        const bool fwd = need_fwd(c);
+        if (fwd_phase) return fwd ? lb_forward<NTL>(c, L) : VJP_OK;
+        const bool ys = c.ys != nullptr;
+        constexpr bool RS = Op::kRevNeedsRs;
+        if constexpr (std::is_same<Op, vjpk::OpAdd>::value) {
+            if (!ys) return launch_lb<NTL, SL, false, false, false>(c, L);
+        }
+        return ys ? launch_lb<NTL, SL, true, true, RS>(c, L) : launch_lb<NTL, SL, true, false, RS>(c, L);
+    }
+    static vjp_status phase_lb(const ScanCall &c, bool fwd_phase) {
+        switch (scan_tune().lb_variant) {
+        case 1: return run_lb<128, 2>(c, fwd_phase);
+        default: return run_lb<128, 3>(c, fwd_phase);
+        }
     }
 
     // ---------------- general reduce rule, LINREC / MAT2 ----------------
@@ -541,6 +677,7 @@ struct ScanImpl {
     }
 
     static vjp_status partial(const ScanCall &c) {
+        if (use_lb(c)) return phase_lb(c, true);  // the `as`-only forward pre-pass K_F (nothing for scan(+))
         if constexpr (Op::kRevNeedsRs) {
             if (use_rs_chunked(c)) return partial_rs(c);
         }
@@ -566,6 +703,7 @@ struct ScanImpl {
     }
 
     static vjp_status finish(const ScanCall &c) {
+        if (use_lb(c)) return phase_lb(c, false);
         if constexpr (Op::kRevNeedsRs) {
             if (use_rs_chunked(c)) return finish_rs(c);
         }
@@ -607,6 +745,11 @@ vjp_status scan_dispatch(int phase, const ScanCall &c, size_t *out) {
     if (phase == kScanPartialBytes) {
         *out = (size_t)(Op::W + Op::kMapD) * 8;
         return VJP_OK;
+    }
+    if (phase == kScanIdentity) {  // an empty shard's record: neutral element, identity map
+        vjpk::scan_identity_record<Op><<<1, 32, 0, c.stream>>>(static_cast<double *>(c.partial));
+        count_launch();
+        return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
     }
     if (c.dtype == VJP_F64) {
         using I = ScanImpl<Op, double>;

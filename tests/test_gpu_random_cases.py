@@ -46,12 +46,13 @@ def test_random_scan(case):
     op = rng.choice(list(W))
     dt = rng.choice([np.float64, np.float32])
     n = rng.choice([1, 2, 3, rng.randint(4, 300), rng.randint(300, 5000), rng.randint(5000, 60000)])
-    path = rng.choice(["default", "chunked", "sweep", "lookback"])
+    path = rng.choice(["default", "chunked", "sweep", "lookback", "blocklb"])
     acc = rng.random() < 0.3
     a, yb = scan_inputs(op, n, dt, 50 + case)
     if a is None and path == "lookback":
         path = "default"
-    kw = {"chunked": path == "chunked", "sweep": path == "sweep", "lookback": path == "lookback"}
+    kw = {"chunked": path == "chunked", "sweep": path == "sweep", "lookback": path == "lookback",
+          "blocklb": path == "blocklb"}
     base = synth.uniform(n * W[op], 77, dtype=TD[dt]) if acc else None
     ref = oracle.vjp_scan(op, yb.numpy(), None if a is None else a.numpy(),
                           out=None if base is None else base.numpy().copy(), accumulate=acc)

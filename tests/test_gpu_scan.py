@@ -46,10 +46,10 @@ def make(op, n, dt, device="cpu"):
     raise ValueError(op)
 
 
-def run_both(op, n, dt, lookback=False, sweep=False):
+def run_both(op, n, dt, lookback=False, sweep=False, **kw):
     a, yb = make(op, n, dt)
     ref = oracle.vjp_scan(op, yb.numpy(), None if a is None else a.numpy())
-    got = vjp.scan(op, yb.to(DEV), None if a is None else a.to(DEV), lookback=lookback, sweep=sweep)
+    got = vjp.scan(op, yb.to(DEV), None if a is None else a.to(DEV), lookback=lookback, sweep=sweep, **kw)
     torch.cuda.synchronize()
     return got.cpu().numpy(), ref
 
@@ -82,10 +82,23 @@ def test_scan_parity_sweep_path(op, dt):
         assert_close(got, ref, dt, what=f"sweep {op} n={n}")
 
 
-@pytest.mark.parametrize("op", ["add", "linrec"])
-def test_scan_sweep_accumulate_ys_and_rounds(op, monkeypatch):
-    """sweep with ACCUMULATE and with ys, and with several tiles per CTA per
-    round and a 2-round look-ahead (VJP_SWEEP_K / VJP_SWEEP_D)."""
+@pytest.mark.parametrize("dt", [np.float64, np.float32], ids=["f64", "f32"])
+@pytest.mark.parametrize("op", ["add", "mul", "min", "max", "linrec", "mat2"])
+def test_scan_parity_blocklb_path(op, dt):
+    """the one-read block look-back (VJP_SCAN_BLOCKLB; scan_blocklb.cuh):
+    one partial tile, one block, many blocks with several look-back windows of
+    32 descriptors, ragged last tiles."""
+    for n in (1, 33, 1023, 4097, 100_003, 1_000_001, 3_000_017, 9_000_011):
+        got, ref = run_both(op, n, dt, blocklb=True)
+        assert_close(got, ref, dt, what=f"blocklb {op} n={n}")
+
+
+@pytest.mark.parametrize("path", ["sweep", "blocklb"])
+@pytest.mark.parametrize("op", ["add", "linrec", "mat2", "min"])
+def test_scan_one_read_paths_accumulate_ys(op, path):
+    """the one-read paths with ACCUMULATE and with ys."""
+    if op == "min" and path == "sweep":
+        pytest.skip("the sweep handles rs-independent maps only")
     n = 2_000_003
     a, yb = make(op, n, np.float64)
     if a is None:
@@ -93,16 +106,41 @@ def test_scan_sweep_accumulate_ys_and_rounds(op, monkeypatch):
     base = synth.uniform(n * WIDTH[op], 12, dtype=torch.float64)
     ref_acc = oracle.vjp_scan(op, yb.numpy(), a.numpy(), out=base.numpy().copy(), accumulate=True)
     ref, ref_ys = oracle.vjp_scan(op, yb.numpy(), a.numpy(), want_ys=True)
-    for k, d in (("", ""), ("3", "1"), ("8", "2")):
-        monkeypatch.setenv("VJP_SWEEP_K", k)
-        monkeypatch.setenv("VJP_SWEEP_D", d)
-        out = base.to(DEV)
-        vjp.scan(op, yb.to(DEV), a.to(DEV), out=out, accumulate=True, sweep=True)
-        assert_close(out.cpu().numpy(), ref_acc, np.float64, what=f"sweep acc {op} K={k} D={d}")
-        got, ys = vjp.scan(op, yb.to(DEV), a.to(DEV), want_ys=True, sweep=True)
-        assert_close(got.cpu().numpy(), ref, np.float64, what=f"sweep {op} K={k} D={d}")
-        if op == "add":
-            assert_close(ys.cpu().numpy(), ref_ys, np.float64, what=f"sweep ys {op}")
+    kw = {path: True}
+    out = base.to(DEV)
+    vjp.scan(op, yb.to(DEV), a.to(DEV), out=out, accumulate=True, **kw)
+    assert_close(out.cpu().numpy(), ref_acc, np.float64, what=f"{path} acc {op}")
+    got, ys = vjp.scan(op, yb.to(DEV), a.to(DEV), want_ys=True, **kw)
+    assert_close(got.cpu().numpy(), ref, np.float64, what=f"{path} {op}")
+    # (LINREC's C = prod c underflows towards 0 at this length: absolute scale 1e-290 there)
+    assert_close(ys.cpu().numpy(), ref_ys, np.float64, scale=np.full(ref_ys.size, 1e-290), what=f"{path} ys {op}")
+
+
+def test_scan_tuning_knobs_subprocess():
+    """the process-wide tuning knobs (read once at first use, vjp.h): several
+    sweep tiles per CTA per round, a 2-round look-ahead, and block look-back
+    blocks of 1 tile (many look-back windows) still match the oracle."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path.insert(0, '.'); sys.path.insert(0, 'tests')\n"
+        "import numpy as np, torch, oracle, synth, paper_2202_10297_b200 as vjp\n"
+        "from _parity import assert_close\n"
+        "for op in ('add', 'linrec'):\n"
+        "    n = 2_000_003\n"
+        "    a, yb = (None, synth.scan_add_seed(n)) if op == 'add' else synth.linrec_inputs(n)\n"
+        "    ref = oracle.vjp_scan(op, yb.numpy(), None if a is None else a.numpy())\n"
+        "    for kw in ({'sweep': True}, {'blocklb': True}):\n"
+        "        got = vjp.scan(op, yb.cuda(), None if a is None else a.cuda(), **kw).cpu().numpy()\n"
+        "        assert_close(got, ref, np.float64, what=f'{op} {kw}')\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for env in ({"VJP_SWEEP_K": "3", "VJP_SWEEP_D": "1", "VJP_LB_L2_MB": "1"},
+                {"VJP_SWEEP_K": "8", "VJP_SWEEP_D": "2", "VJP_LB_L2_MB": "400"}):
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, env={**os.environ, **env},
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
 @pytest.mark.parametrize("dt", [np.float64, np.float32], ids=["f64", "f32"])
@@ -111,7 +149,7 @@ def test_scan_add_integer_seeds_bit_exact(dt):
     for n in (10_000, 1 << 20, (1 << 20) + 3, 5_000_011):
         yb = synth.scan_add_seed(n, kind="int", dtype=TD[dt])
         ref = oracle.vjp_scan("add", yb.numpy(), None)
-        for kw in ({}, {"lookback": True}, {"sweep": True}, {"chunked": True}):
+        for kw in ({}, {"lookback": True}, {"sweep": True}, {"chunked": True}, {"blocklb": True}):
             got = vjp.scan("add", yb.to(DEV), **kw).cpu().numpy()
             assert np.array_equal(got, ref), kw
 
