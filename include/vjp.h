@@ -237,19 +237,30 @@ vjp_status vjp_reduce_finish(vjp_op op, vjp_dtype dtype, int64_t n, const void *
  * sweep: the reduce rule with y_bar replaced by hs_bar[inds[i]]:
  *   ADD : as_bar_i = hs_bar[b_i] (a gather; `as` may be NULL).
  *   MUL : per-bin (p_b, z_b) forward histogram, then the three cases of
- *         vjp_reduce per bin.
+ *         vjp_reduce per bin.  p_b is accumulated as an exact integer sum of
+ *         64-bit fixed-point log2|a| codes (sign folded in; DESIGN 7.4), so
+ *         it does not depend on the order of the additions; relative error
+ *         <= 0.7 * 2^-52 * (factors in the bin).
  *   MIN/MAX : per-bin winner (value, lowest index), as_bar = 0 except
  *         as_bar[winner_b] = hs_bar[b] (ACCUMULATE: only the winners).
+ * VECTORISED operators (width > 1, "elementwise", reading A24):
+ * element i is the row as[i][0..width), bin b the row hs[b][0..width); every
+ * rule applies per component j — (b, j) has its own (p, z) and its own
+ * lowest-index winner.  width = 1 is the hot path (config 4).
  * The general operator ("work is in progress") and LINREC/MAT2
- * return VJP_EUNSUPPORTED.
- *   inds   [n] int32/int64 bins;  as [n];  hs_bar [m];  as_bar [n] output.
- *   hs     nullable DEVICE [m]: primal histogram (ADD: sum, MUL: product,
- *          MIN/MAX: extremum, +-inf for an empty bin).
- *   winners nullable DEVICE int64[m]: MIN/MAX winner index (-1 empty bin),
- *          MUL: zero count per bin.
+ * return VJP_EUNSUPPORTED (see vjp_reduce_by_index_general for MUL).
+ *   inds   [n] int32/int64 bins;  as [n x width];  hs_bar [m x width];
+ *   as_bar [n x width] output.
+ *   hs     nullable DEVICE [m x width]: primal histogram (ADD: sum by
+ *          atomic adds — rounding order-dependent; MUL: product; MIN/MAX:
+ *          extremum, +-inf for an empty (bin, component)).
+ *   winners nullable DEVICE int64[m x width]: MIN/MAX winner ELEMENT index
+ *          (-1 empty), MUL: zero count, ADD: -1.
+ * Errors: VJP_EINVAL (width < 1, m < 1, NULL inputs), VJP_EUNSUPPORTED
+ * (LINREC/MAT2), VJP_EALIGN, VJP_EWORKSPACE, VJP_ECUDA.
  * ==================================================================== */
-size_t vjp_reduce_by_index_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_t n, int64_t m);
-vjp_status vjp_reduce_by_index(vjp_op op, vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m,
+size_t vjp_reduce_by_index_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_t n, int64_t m, int64_t width);
+vjp_status vjp_reduce_by_index(vjp_op op, vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, int64_t width,
                                const void *inds, const void *as, const void *hs_bar,
                                void *as_bar, void *hs, int64_t *winners, void *ws,
                                size_t ws_bytes, vjp_stream_t stream, unsigned flags);
@@ -272,11 +283,16 @@ vjp_status vjp_reduce_by_index_general(vjp_op op, vjp_dtype dtype, vjp_itype ity
                                        void *as_bar, void *ws, size_t ws_bytes, vjp_stream_t stream,
                                        unsigned flags);
 
-/* Multi-GPU split (partition by input range; per-bin state all-reduced):
- *   partial: per-bin state of the local shard into bin_val (DEVICE double[m])
- *            and bin_aux (DEVICE int64[m]):
- *              MUL     bin_val = product of nonzeros, bin_aux = zero count
- *                      -> all_reduce PRODUCT(bin_val), SUM(bin_aux)
+/* Multi-GPU split (partition by input range; per-bin state all-reduced;
+ * width 1; the workspace is vjp_reduce_by_index_workspace_bytes(.., 1)):
+ *   partial: per-bin state of the local shard into bin_val (DEVICE, 8 bytes
+ *            per bin) and bin_aux (DEVICE int64[m]):
+ *              MUL     bin_val = int64 code sum of the shard's nonzero factors
+ *                      (bit pattern stored in the 8-byte slot; code(a) =
+ *                      round(log2|a| 2^51) + [a < 0] 2^63 mod 2^64, DESIGN 7.4),
+ *                      bin_aux = zero count
+ *                      -> all_reduce SUM over int64 of both (exact: integer
+ *                         adds mod 2^64, independent of order and of world)
  *              MIN/MAX bin_val = local extremum (+-inf if empty), bin_aux =
  *                      lowest GLOBAL index reaching it (INT64_MAX if empty)
  *                      -> all_reduce MIN/MAX(bin_val), then

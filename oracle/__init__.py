@@ -133,9 +133,40 @@ def vjp_reduce(op, as_: np.ndarray, y_bar, *, out=None, accumulate: bool = False
 
 
 def vjp_reduce_by_index(op, inds: np.ndarray, as_: np.ndarray | None, hs_bar: np.ndarray, *,
-                        out=None, accumulate: bool = False):
+                        out=None, accumulate: bool = False, width: int = 1):
     """Returns (as_bar, hs, winners, zeros) for hs = reduce_by_index op m inds as_
-    (P:1098-1126), m = len(hs_bar)."""
+    (P:1098-1126), m = len(hs_bar) / width.
+
+    width > 1 (vectorised operator): the operator acts elementwise on rows
+    (P:1229-1231), so by definition component j of every row is its own
+    scalar reduce_by_index over the same bins (reading A24) — the scalar oracle
+    is run once per component and the results are laid out [n x width] /
+    [m x width]."""
+    if width > 1:
+        inds = np.ascontiguousarray(inds)
+        n = inds.size
+        hb2 = np.asarray(hs_bar).reshape(-1, width)
+        a2 = None if as_ is None else np.asarray(as_).reshape(n, width)
+        ab = np.zeros((n, width), dtype=hb2.dtype)
+        if out is not None:
+            ab[...] = np.asarray(out).reshape(n, width)
+        hs = np.zeros_like(hb2) if as_ is not None else None
+        win = np.zeros(hb2.shape, dtype=np.int64)
+        zer = np.zeros(hb2.shape, dtype=np.int64)
+        for j in range(width):
+            col = np.ascontiguousarray(ab[:, j])
+            r = vjp_reduce_by_index(op, inds, None if a2 is None else np.ascontiguousarray(a2[:, j]),
+                                    np.ascontiguousarray(hb2[:, j]), out=col, accumulate=accumulate)
+            ab[:, j] = r[0]
+            if hs is not None:
+                hs[:, j] = r[1]
+            win[:, j] = r[2]
+            zer[:, j] = r[3]
+        flat = ab.reshape(-1)
+        if out is not None:
+            np.asarray(out).reshape(-1)[...] = flat
+            flat = out
+        return flat, None if hs is None else hs.reshape(-1), win.reshape(-1), zer.reshape(-1)
     o = _op(op)
     inds = np.ascontiguousarray(inds)
     hs_bar = np.ascontiguousarray(hs_bar)

@@ -74,8 +74,8 @@ def lib():
             "vjp_reduce_partial_bytes": ([], sz),
             "vjp_reduce_partial": ([ci, ci, i64, vp, vp, sz, sp, vp, vp], ci),
             "vjp_reduce_finish": ([ci, ci, i64, vp, vp, vp, vp, vp, vp, sz, sp, vp, vp, u32], ci),
-            "vjp_reduce_by_index_workspace_bytes": ([ci, ci, i64, i64], sz),
-            "vjp_reduce_by_index": ([ci, ci, ci, i64, i64, vp, vp, vp, vp, vp, vp, vp, sz, vp, u32], ci),
+            "vjp_reduce_by_index_workspace_bytes": ([ci, ci, i64, i64, i64], sz),
+            "vjp_reduce_by_index": ([ci, ci, ci, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp, sz, vp, u32], ci),
             "vjp_reduce_by_index_partial": ([ci, ci, ci, i64, i64, vp, vp, vp, sz, sp, vp, vp, vp], ci),
             "vjp_reduce_by_index_select": ([ci, i64, vp, vp, vp, vp], ci),
             "vjp_reduce_by_index_finish": ([ci, ci, ci, i64, i64, vp, vp, vp, vp, vp, vp, vp, sz, sp, vp, u32], ci),
@@ -296,26 +296,32 @@ def reduce(op, as_: torch.Tensor, y_bar, *, out: torch.Tensor | None = None, wan
 
 def reduce_by_index(op, inds: torch.Tensor, as_: torch.Tensor | None, hs_bar: torch.Tensor, *,
                     out: torch.Tensor | None = None, want_hs: bool = False, accumulate: bool = False,
-                    general: bool = False):
-    """as_bar of ``hs = reduce_by_index op m inds as_`` with m = len(hs_bar)
+                    general: bool = False, width: int = 1):
+    """as_bar of ``hs = reduce_by_index op m inds as_`` with m = len(hs_bar) / width
     (sec 5.1.2).  Returns as_bar, or (as_bar, hs, winners) if want_hs
     (winners: MIN/MAX per-bin winner index, -1 for an empty bin; MUL: zero count).
-    general=True (MUL only): the paper's general rule, counting sort + per-bin
-    exclusive product scans (vjp_reduce_by_index_general)."""
+    width > 1: vectorised operator, as_ is [n x width] and
+    hs_bar [m x width] (flat or 2-D), rules per component (reading A24).
+    general=True (MUL, width 1): the paper's general rule, counting sort +
+    per-bin exclusive product scans (vjp_reduce_by_index_general)."""
     o = _op(op)
     host = not inds.is_cuda
     dev = _dev_of(inds, as_, hs_bar, out)
     ix = _to(inds, dev)
     a = _to(as_, dev)
     hb = _to(hs_bar, dev)
-    n, m = ix.numel(), hb.numel()
-    if a is not None and (a.dtype != hb.dtype or a.numel() != n):
-        raise ValueError("as_ must have len(inds) elements of hs_bar's dtype")
-    ab = _out_buf(out, torch.empty(n, dtype=hb.dtype, device=dev), dev, accumulate)
-    hs = torch.empty(m, dtype=hb.dtype, device=dev) if want_hs else None
-    win = torch.empty(m, dtype=torch.int64, device=dev) if want_hs else None
+    if width < 1 or hb.numel() % width:
+        raise ValueError("width must be >= 1 and divide hs_bar's size")
+    n, m = ix.numel(), hb.numel() // width
+    if a is not None and (a.dtype != hb.dtype or a.numel() != n * width):
+        raise ValueError("as_ must have len(inds) * width elements of hs_bar's dtype")
+    ab = _out_buf(out, torch.empty(n * width, dtype=hb.dtype, device=dev), dev, accumulate)
+    hs = torch.empty(m * width, dtype=hb.dtype, device=dev) if want_hs else None
+    win = torch.empty(m * width, dtype=torch.int64, device=dev) if want_hs else None
     L = lib()
     if general:
+        if width != 1:
+            raise ValueError("general=True supports width 1")
         if want_hs:
             raise ValueError("general=True returns the adjoint only")
         ws = workspace(L.vjp_reduce_by_index_general_workspace_bytes(o, _dt(hb), n, m), dev)
@@ -327,8 +333,8 @@ def reduce_by_index(op, inds: torch.Tensor, as_: torch.Tensor | None, hs_bar: to
             torch.cuda.current_stream(dev).synchronize()
             return out
         return _host_out(ab, host)
-    ws = workspace(L.vjp_reduce_by_index_workspace_bytes(o, _dt(hb), n, m), dev)
-    _check(L.vjp_reduce_by_index(o, _dt(hb), _it(ix), n, m, _p(ix), _p(a), _p(hb), _p(ab), _p(hs), _p(win),
+    ws = workspace(L.vjp_reduce_by_index_workspace_bytes(o, _dt(hb), n, m, width), dev)
+    _check(L.vjp_reduce_by_index(o, _dt(hb), _it(ix), n, m, width, _p(ix), _p(a), _p(hb), _p(ab), _p(hs), _p(win),
                                  _p(ws), 0 if ws is None else ws.numel(), _stream(dev),
                                  ACCUMULATE if accumulate else 0),
            "vjp_reduce_by_index")

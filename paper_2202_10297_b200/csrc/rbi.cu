@@ -81,8 +81,8 @@ struct RbiParams {
     double *p;        // MUL: [m] product of nonzeros
     unsigned long long *z;  // MUL: [m] zero count
     Win *win;         // MIN/MAX: [m] {value key (max), ~index (max)}
-    unsigned long long *ng;     // MUL, log domain: [m] count of negative factors
-    int32_t log_domain, pad2;   // MUL, large m: p holds sum log2|a| until finalised
+    unsigned long long *code;   // MUL: [m] sum of the factors' codes (mod 2^64), aliases p
+    int32_t log_domain, pad2;   // MUL: p holds the codes until rbi_log_finalize
     unsigned long long *cand;   // MIN/MAX: candidate list [cap][3] = {key, global index, bin}
     unsigned long long *ncand;  // candidate counter
     int64_t cap;
@@ -94,9 +94,8 @@ __global__ void rbi_init(RbiParams P) {
     if (blockIdx.x == 0 && threadIdx.x == 0 && P.ncand) *P.ncand = 0ull;
     for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < P.m; b += (int64_t)gridDim.x * blockDim.x) {
         if (OP == VJP_MUL) {
-            P.p[b] = P.log_domain ? 0.0 : 1.0;
+            P.code[b] = 0ull;
             P.z[b] = 0ull;
-            if (P.log_domain) P.ng[b] = 0ull;
         }
         else { P.win[b].key = 0ull; P.win[b].inv = 0ull; }
     }
@@ -219,14 +218,14 @@ __device__ __forceinline__ void rbi_stream(const I *__restrict__ inds, const T *
     }
 }
 
-// log2|x| for finite x != 0 (the MUL histograms' log domain), without the
-// library routine's special-case paths: x = m * 2^e with m in [sqrt(1/2),
-// sqrt(2)), ln m = 2 atanh(s), s = (m - 1)/(m + 1) (|s| <= 0.1716; m - 1 is
-// exact by Sterbenz), atanh(s)/s = sum_k s^(2k)/(2k+1) to k = 11 (truncation
-// < 1e-18).  Error: a few ulp of log2 m plus one rounding of e + log2 m —
-// the same order as log2() (measured against log2() in
-// tests/test_gpu_rbi.py::test_rbi_mul_log2_accuracy).  Denormals are rescaled.
-__device__ __forceinline__ double log2_abs(double x) {
+// log2|x| = e + l for finite x != 0 (the MUL histograms' log domain), without
+// the library routine's special-case paths: x = m * 2^e with m in [sqrt(1/2),
+// sqrt(2)), l = log2 m = (2/ln 2) atanh(s), s = (m - 1)/(m + 1) (|s| <= 0.1716;
+// m - 1 is exact by Sterbenz), atanh(s)/s = sum_k s^(2k)/(2k+1) to k = 11
+// (truncation < 1e-18).  |l| <= 1/2, error a few ulp of l (measured against
+// log2() in tests/test_gpu_rbi.py::test_rbi_mul_log2_accuracy).  Denormals are
+// rescaled.
+__device__ __forceinline__ double log2_split(double x, int &e_out) {
     long long b = __double_as_longlong(x) & 0x7fffffffffffffffll;
     int e = (int)(b >> 52);
     if (e == 0) {  // subnormal
@@ -264,8 +263,40 @@ __device__ __forceinline__ double log2_abs(double x) {
     const double t = s * s2 * p;  // atanh(s) - s
     // log2 m = 2 (s + t) / ln 2, with 2/ln 2 split hi + lo for the dominant term
     const double k_hi = 2.8853900817779268, k_lo = 4.0710547481862066e-17;
-    const double l = fma(s, k_hi, fma(s, k_lo, t * k_hi));
+    e_out = e;
+    return fma(s, k_hi, fma(s, k_lo, t * k_hi));
+}
+__device__ __forceinline__ double log2_abs(double x) {
+    int e;
+    const double l = log2_split(x, e);
     return (double)e + l;
+}
+
+// The MUL histograms accumulate, per bin, ONE 64-bit integer code per
+// nonzero factor a (reading R13b, DESIGN 7.4):
+//     code(a) = round(log2|a| * 2^51)  +  (a < 0 ? 2^63 : 0)      (mod 2^64)
+// Sums of codes are taken mod 2^64 with integer adds, so they are EXACT and
+// independent of the order of the additions (deterministic, and the
+// multi-GPU exchange is an integer SUM).  Decoding a bin's total T: the log
+// sum L = T sign-extended from 63 bits (|L| < 2^62 because |sum log2|a|| <
+// 2048 in the domain where p stays finite and normal, reading R13), the sign
+// parity = bit 63 of (T - L); p = (-1)^parity * 2^(L / 2^51).  Quantisation
+// error 2^-52 per factor on log2, i.e. <= 0.7 * 2^-52 * n_b relative on p
+// (n_b = factors in the bin): 4e-11 at n_b = 2.7e5 (config 4, m = 10^3).
+__device__ __forceinline__ unsigned long long mul_code(double x) {
+    int e;
+    const double l = log2_split(x, e);  // |l| <= 1/2: l * 2^51 exact in f64
+    const long long q = ((long long)e << 51) + __double2ll_rn(l * 0x1p51);
+    return (unsigned long long)q + (x < 0.0 ? 0x8000000000000000ull : 0ull);
+}
+__device__ __forceinline__ double mul_decode(unsigned long long T) {
+    const long long L = ((long long)(T << 1)) >> 1;  // sign-extend 63 bits
+    const bool neg = (((T - (unsigned long long)L) >> 63) & 1ull) != 0;
+    const long long E = L >> 51;                      // floor(L / 2^51)
+    const double f = (double)(L & ((1ll << 51) - 1)) * 0x1p-51;  // [0, 1), exact
+    double v = exp2(f);
+    v = (E > 2100) ? INFINITY : (E < -2100 ? 0.0 : ldexp(v, (int)E));
+    return neg ? -v : v;
 }
 
 // test hook: log2_abs on n values (tests compare it with log2 on the device)
@@ -275,61 +306,57 @@ __global__ void rbi_log2_probe(const double *x, double *y, int64_t n) {
 }
 
 // MUL, large m: every element must contribute, and a CAS-multiply costs two
-// dependent L2 round trips per element.  Instead accumulate log2|a| with
-// fire-and-forget f64 red.add, count zeros and negative factors, and finalise
-// p_b = (-1)^neg * exp2(sum) per bin.  Error: <= 1 ulp per log2 plus the
-// summation order, i.e. ~ n_b * u * max|log2 a| relative (~3e-13 for
-// |log2 a| ~ 10 and n_b = 268) — inside the 1e-10 tolerance; the domain
-// assumption R13 (p finite and normal) is unchanged.
+// dependent L2 round trips per element.  Instead add each factor's 64-bit
+// code (above) into the bin with a fire-and-forget integer red.add (native
+// RED.ADD.64 in L2) and count zeros.
 template <class T, class I>
 __global__ void __launch_bounds__(kBThreads) rbi_fwd_log(const I *__restrict__ inds, const T *__restrict__ as,
                                                          RbiParams P) {
     rbi_stream<T, I>(inds, as, nullptr, P, [&](int64_t b, double x, int64_t, bool ok) {
         if (!ok) return;
-        if (x == 0.0) {
-            atomicAdd(P.z + b, 1ull);
-        } else {
-            atomicAdd(P.p + b, log2_abs(x));
-            if (x < 0.0) atomicAdd(P.ng + b, 1ull);
-        }
+        if (x == 0.0) atomicAdd(P.z + b, 1ull);
+        else atomicAdd(P.code + b, mul_code(x));
     });
 }
-// small m, log domain: one shared-memory table per CTA (sum log2|a|, zero and
-// negative counts) updated with shared-memory reductions, merged with global
-// reductions (measured faster than warp-private product tables with
-// owner-table conflict resolution: 2.42 vs 2.72 ms at m = 10^3, and it keeps
-// full occupancy at larger m)
+// small m: one shared-memory table per CTA.  Shared-memory atomics are native
+// only for 32-bit integer add on sm_100a (f64 and 64-bit adds compile to
+// ATOMS.CAST.SPIN.64 CAS loops, profiles/r01_ncu_full_rbi_fwd_smem_log_m1e3.txt),
+// so each 64-bit code is added as two 32-bit words: the low word with
+// ATOMS.ADD returning the old value (a wrap is a carry into the high word),
+// the high word with ATOMS.ADD — exact mod 2^64.  Zero counts: 32-bit adds.
+// Merged into the global codes with RED.ADD.64.
 template <class T, class I>
 __global__ void __launch_bounds__(kBThreads, kBMinBlocks) rbi_fwd_smem_log(const I *__restrict__ inds, const T *__restrict__ as,
                                                               RbiParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
-    double *lg = reinterpret_cast<double *>(smem);
-    unsigned *zc = reinterpret_cast<unsigned *>(lg + P.m);
-    unsigned *nc = zc + P.m;
-    for (int64_t b = threadIdx.x; b < P.m; b += blockDim.x) { lg[b] = 0.0; zc[b] = 0u; nc[b] = 0u; }
+    unsigned *lo = reinterpret_cast<unsigned *>(smem);
+    unsigned *hi = lo + P.m;
+    unsigned *zc = hi + P.m;
+    for (int64_t b = threadIdx.x; b < P.m; b += blockDim.x) { lo[b] = 0u; hi[b] = 0u; zc[b] = 0u; }
     __syncthreads();
     rbi_stream<T, I>(inds, as, nullptr, P, [&](int64_t b, double x, int64_t, bool ok) {
         if (!ok) return;
         if (x == 0.0) {
             atomicAdd(zc + b, 1u);
         } else {
-            atomicAdd(lg + b, log2_abs(x));
-            if (x < 0.0) atomicAdd(nc + b, 1u);
+            const unsigned long long q = mul_code(x);
+            const unsigned ql = (unsigned)q;
+            const unsigned old = atomicAdd(lo + b, ql);
+            atomicAdd(hi + b, (unsigned)(q >> 32) + (old + ql < old ? 1u : 0u));
         }
     });
     __syncthreads();
     for (int64_t b = threadIdx.x; b < P.m; b += blockDim.x) {
-        if (lg[b] != 0.0) atomicAdd(P.p + b, lg[b]);
+        const unsigned long long t = ((unsigned long long)hi[b] << 32) | lo[b];
+        if (t) atomicAdd(P.code + b, t);
         if (zc[b]) atomicAdd(P.z + b, (unsigned long long)zc[b]);
-        if (nc[b]) atomicAdd(P.ng + b, (unsigned long long)nc[b]);
     }
 }
 
+// p_b from the bin's code (in place: P.p aliases P.code)
 __global__ void rbi_log_finalize(RbiParams P) {
-    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < P.m; b += (int64_t)gridDim.x * blockDim.x) {
-        const double v = exp2(P.p[b]);
-        P.p[b] = (P.ng[b] & 1ull) ? -v : v;
-    }
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < P.m; b += (int64_t)gridDim.x * blockDim.x)
+        P.p[b] = mul_decode(P.code[b]);
 }
 
 __device__ __forceinline__ void red_max_u64(unsigned long long *a, unsigned long long v) {
@@ -563,8 +590,8 @@ template <int OP>
 __global__ void rbi_export(const RbiParams P, double *bin_val, int64_t *bin_aux) {
     const bool is_min = OP == VJP_MIN;
     for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < P.m; b += (int64_t)gridDim.x * blockDim.x) {
-        if (OP == VJP_MUL) {
-            bin_val[b] = P.p[b];
+        if (OP == VJP_MUL) {  // the bin's code sum (int64 bits; combined by integer SUM) and zero count
+            reinterpret_cast<unsigned long long *>(bin_val)[b] = P.code[b];
             bin_aux[b] = (int64_t)P.z[b];
         } else {
             const Win w = P.win[b];
@@ -581,7 +608,8 @@ template <class T>
 __global__ void rbi_mul_prep_ext(const T *__restrict__ hs_bar, const double *__restrict__ bin_val,
                                  const int64_t *__restrict__ bin_aux, MulPack<T> *pk, int64_t m) {
     for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < m; b += (int64_t)gridDim.x * blockDim.x) {
-        pk[b].q = (double)hs_bar[b] * bin_val[b];
+        const double pb = mul_decode(reinterpret_cast<const unsigned long long *>(bin_val)[b]);
+        pk[b].q = (double)hs_bar[b] * pb;
         pk[b].z = bin_aux[b];
     }
 }
@@ -601,6 +629,152 @@ __global__ void __launch_bounds__(kBThreads) rbi_ext_gather(const I *__restrict_
     }
 }
 
+
+// =============================================================================
+// width > 1: vectorised operators ("elementwise"; reading A24):
+// element i is the row as[i][0..w), bin b the row hs[b][0..w), and the rules
+// apply per component j — (bin, component) (b, j) is an independent scalar
+// bin with its own (p, z) for MUL and its own lowest-index winner for MIN/MAX.
+// Rows are handled by groups of GW = min(32, pow2 >= w) lanes (no division:
+// the group loops over rows, its lanes over the row's components), so a row
+// of w >= 32 components is read and written coalesced.  Per-(bin, component)
+// state lives in the same workspace arrays as width 1, indexed b * w + j.
+// =============================================================================
+struct WideGeo {
+    int64_t n, m, w;
+    int32_t gw, pad;  // lanes per row group
+};
+__device__ __forceinline__ void wide_start(const WideGeo &g, int64_t &row, int64_t &rstride, int &lane) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    row = t / g.gw;
+    lane = (int)(t % g.gw);
+    rstride = ((int64_t)gridDim.x * blockDim.x) / g.gw;
+}
+
+template <class T, class I>
+__global__ void __launch_bounds__(kBThreads) rbiw_add_bwd(const I *__restrict__ inds, const T *__restrict__ hs_bar,
+                                                          T *__restrict__ ab, WideGeo g, int acc) {
+    int64_t i, rs;
+    int lane;
+    wide_start(g, i, rs, lane);
+    for (; i < g.n; i += rs) {
+        const int64_t b = (int64_t)__ldg(inds + i);
+        const bool ok = b >= 0 && b < g.m;
+        for (int64_t j = lane; j < g.w; j += g.gw) {
+            const double v = ok ? (double)__ldg(hs_bar + b * g.w + j) : 0.0;
+            T *d = ab + i * g.w + j;
+            if (acc) { if (ok) *d = (T)((double)*d + v); }
+            else *d = (T)v;
+        }
+    }
+}
+template <class T, class I>
+__global__ void __launch_bounds__(kBThreads) rbiw_add_hist(const I *__restrict__ inds, const T *__restrict__ as,
+                                                           T *__restrict__ hs, WideGeo g) {
+    int64_t i, rs;
+    int lane;
+    wide_start(g, i, rs, lane);
+    for (; i < g.n; i += rs) {
+        const int64_t b = (int64_t)__ldg(inds + i);
+        if (b < 0 || b >= g.m) continue;
+        for (int64_t j = lane; j < g.w; j += g.gw) atomicAdd(hs + b * g.w + j, __ldg(as + i * g.w + j));
+    }
+}
+// MUL forward: per (bin, component) code sums and zero counts (L2 reductions)
+template <class T, class I>
+__global__ void __launch_bounds__(kBThreads) rbiw_mul_fwd(const I *__restrict__ inds, const T *__restrict__ as,
+                                                          RbiParams P, WideGeo g) {
+    int64_t i, rs;
+    int lane;
+    wide_start(g, i, rs, lane);
+    for (; i < g.n; i += rs) {
+        const int64_t b = (int64_t)__ldg(inds + i);
+        if (b < 0 || b >= g.m) continue;
+        for (int64_t j = lane; j < g.w; j += g.gw) {
+            const double x = (double)__ldg(as + i * g.w + j);
+            if (x == 0.0) atomicAdd(P.z + b * g.w + j, 1ull);
+            else atomicAdd(P.code + b * g.w + j, mul_code(x));
+        }
+    }
+}
+template <class T, class I>
+__global__ void __launch_bounds__(kBThreads) rbiw_mul_bwd(const I *__restrict__ inds, const T *__restrict__ as,
+                                                          const MulPack<T> *__restrict__ pk, T *__restrict__ ab,
+                                                          WideGeo g, int acc) {
+    int64_t i, rs;
+    int lane;
+    wide_start(g, i, rs, lane);
+    for (; i < g.n; i += rs) {
+        const int64_t b = (int64_t)__ldg(inds + i);
+        const bool ok = b >= 0 && b < g.m;
+        for (int64_t j = lane; j < g.w; j += g.gw) {
+            const double a = (double)__ldg(as + i * g.w + j);
+            double v = 0.0;
+            bool touch = false;
+            if (ok) {
+                const double2 k = __ldg(reinterpret_cast<const double2 *>(pk + b * g.w + j));
+                const int64_t z = (int64_t)__double_as_longlong(k.y);
+                if (z == 0) { touch = true; v = k.x / a; }              // P:1043-1046 per (bin, component)
+                else if (z == 1 && a == 0.0) { touch = true; v = k.x; }
+            }
+            T *d = ab + i * g.w + j;
+            if (acc) { if (touch) *d = (T)((double)*d + v); }
+            else *d = (T)v;
+        }
+    }
+}
+// MIN/MAX: phase A (value keys, red.max behind the monotone filter), phase B
+// (lowest ELEMENT index among the elements reaching the final key), scatter
+template <class T, class I, int OP>
+__global__ void __launch_bounds__(kBThreads) rbiw_ext_a(const I *__restrict__ inds, const T *__restrict__ as,
+                                                        RbiParams P, WideGeo g) {
+    int64_t i, rs;
+    int lane;
+    wide_start(g, i, rs, lane);
+    for (; i < g.n; i += rs) {
+        const int64_t b = (int64_t)__ldg(inds + i);
+        if (b < 0 || b >= g.m) continue;
+        for (int64_t j = lane; j < g.w; j += g.gw) {
+            const uint64_t k = ord_key((double)__ldg(as + i * g.w + j), OP == VJP_MIN);
+            unsigned long long *slot = reinterpret_cast<unsigned long long *>(&P.win[b * g.w + j].key);
+            if (k > __ldcg(slot)) red_max_u64(slot, k);
+        }
+    }
+}
+template <class T, class I, int OP>
+__global__ void __launch_bounds__(kBThreads) rbiw_ext_b(const I *__restrict__ inds, const T *__restrict__ as,
+                                                        RbiParams P, WideGeo g) {
+    int64_t i, rs;
+    int lane;
+    wide_start(g, i, rs, lane);
+    for (; i < g.n; i += rs) {
+        const int64_t b = (int64_t)__ldg(inds + i);
+        if (b < 0 || b >= g.m) continue;
+        for (int64_t j = lane; j < g.w; j += g.gw) {
+            const uint64_t k = ord_key((double)__ldg(as + i * g.w + j), OP == VJP_MIN);
+            Win *wb = P.win + b * g.w + j;
+            if (k == __ldcg(reinterpret_cast<const unsigned long long *>(&wb->key)))
+                red_max_u64(reinterpret_cast<unsigned long long *>(&wb->inv), ~(uint64_t)i);
+        }
+    }
+}
+template <class T, int OP>
+__global__ void rbiw_ext_scatter(const Win *__restrict__ win, const T *__restrict__ hs_bar, T *__restrict__ ab,
+                                 WideGeo g, int acc, T *hs, int64_t *winners) {
+    const bool is_min = OP == VJP_MIN;
+    const int64_t mw = g.m * g.w;
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < mw; q += (int64_t)gridDim.x * blockDim.x) {
+        const Win w = win[q];
+        const int64_t i = w.key ? (int64_t)~w.inv : -1;  // winning element (row) of (b, j)
+        if (winners) winners[q] = i;
+        if (hs) hs[q] = (T)(w.key ? key_val(w.key, is_min) : (is_min ? INFINITY : -INFINITY));
+        if (i >= 0) {
+            T *d = ab + i * g.w + (q % g.w);
+            *d = acc ? (T)((double)*d + (double)hs_bar[q]) : hs_bar[q];
+        }
+    }
+}
+
 }  // namespace vjpk
 
 // =============================================================================
@@ -615,7 +789,7 @@ constexpr int64_t kMaxWarpsA = 65536;  // phase-A warps (per-warp candidate coun
 bool op_ok(vjp_op op) { return op == VJP_ADD || op == VJP_MUL || op == VJP_MIN || op == VJP_MAX; }
 
 struct BLayout {
-    size_t p, z, ng, win, pk, ncand, cand, total;
+    size_t p, z, win, pk, ncand, cand, total;
     int64_t cap;
 };
 // candidate list capacity for MIN/MAX: ~(H(n/m) + ties) per bin are expected;
@@ -631,7 +805,6 @@ BLayout blayout(int64_t m, int64_t n = 0, bool ext = false) {
     size_t off = 0;
     L.p = off; off += vjph::align256(sizeof(double) * (size_t)m);
     L.z = off; off += vjph::align256(sizeof(unsigned long long) * (size_t)m);
-    L.ng = off; off += vjph::align256(sizeof(unsigned long long) * (size_t)m);
     L.win = off; off += vjph::align256(sizeof(Win) * (size_t)m);
     L.pk = off; off += vjph::align256(16 * (size_t)m);
     L.ncand = off; off += vjph::align256(8 * (1 + kMaxWarpsA));
@@ -669,7 +842,7 @@ RbiParams params(int64_t n, int64_t m, int64_t goff, void *ws, unsigned flags, i
     P.p = reinterpret_cast<double *>(w + L.p);
     P.z = reinterpret_cast<unsigned long long *>(w + L.z);
     P.win = reinterpret_cast<Win *>(w + L.win);
-    P.ng = reinterpret_cast<unsigned long long *>(w + L.ng);
+    P.code = reinterpret_cast<unsigned long long *>(w + L.p);  // the codes, decoded in place into p
     P.ncand = reinterpret_cast<unsigned long long *>(w + L.ncand);
     P.cand = reinterpret_cast<unsigned long long *>(w + L.cand);
     P.cap = L.cap;
@@ -679,8 +852,8 @@ RbiParams params(int64_t n, int64_t m, int64_t goff, void *ws, unsigned flags, i
 
 // forward histogram (MUL / MIN / MAX), init included
 template <class T, class I, int OP>
-vjp_status forward(const I *inds, const T *as, T *ab, RbiParams P, cudaStream_t s) {
-    const size_t sm_log = (size_t)P.m * 16;
+vjp_status forward(const I *inds, const T *as, T *ab, RbiParams P, cudaStream_t s, bool finalize = true) {
+    const size_t sm_log = (size_t)P.m * 12;  // low word, high word, zero count
     P.log_domain = (OP == VJP_MUL) ? 1 : 0;
     rbi_init<OP><<<grid_for(P.m, 4), kBThreads, 0, s>>>(P);
     vjph::count_launch();
@@ -695,6 +868,7 @@ vjp_status forward(const I *inds, const T *as, T *ab, RbiParams P, cudaStream_t 
             rbi_fwd_log<T, I><<<grid_resident(rbi_fwd_log<T, I>, work), kBThreads, 0, s>>>(inds, as, P);
         }
         vjph::count_launch();
+        if (!finalize) return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;  // partial: export the codes
         rbi_log_finalize<<<grid_for(P.m, 4), kBThreads, 0, s>>>(P);
     } else {
         const size_t smk = sizeof(unsigned long long) * (size_t)P.m;
@@ -781,7 +955,7 @@ vjp_status run_partial(vjp_op op, int64_t n, int64_t m, int64_t goff, const void
     vjp_status st = VJP_OK;
     const I *ix = static_cast<const I *>(inds);
     const T *a = static_cast<const T *>(as);
-    if (op == VJP_MUL) st = forward<T, I, VJP_MUL>(ix, a, nullptr, P, s);
+    if (op == VJP_MUL) st = forward<T, I, VJP_MUL>(ix, a, nullptr, P, s, false);
     if (op == VJP_MIN) st = forward<T, I, VJP_MIN>(ix, a, nullptr, P, s);
     if (op == VJP_MAX) st = forward<T, I, VJP_MAX>(ix, a, nullptr, P, s);
     if (st != VJP_OK) return st;
@@ -820,6 +994,80 @@ vjp_status run_finish(vjp_op op, int64_t n, int64_t m, int64_t goff, const void 
     return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
 }
 
+
+// width > 1 (vectorised operators, reading A24): per-(bin, component) state
+// in the width-1 workspace layout with m * width bins
+WideGeo wide_geo(int64_t n, int64_t m, int64_t w) {
+    WideGeo g{};
+    g.n = n;
+    g.m = m;
+    g.w = w;
+    int gw = 1;
+    while (gw < w && gw < 32) gw <<= 1;
+    g.gw = gw;
+    return g;
+}
+int grid_wide(const WideGeo &g) {
+    int64_t rows_per_cta = kBThreads / g.gw;
+    int64_t b = (g.n + rows_per_cta - 1) / rows_per_cta;
+    int64_t cap = (int64_t)vjph::sm_count() * 8;
+    if (b > cap) b = cap;
+    return (int)(b < 1 ? 1 : b);
+}
+template <class T, class I>
+vjp_status run_wide(vjp_op op, int64_t n, int64_t m, int64_t w, const void *inds_, const void *as_,
+                    const void *hsb_, void *ab_, void *hs_, int64_t *winners, void *ws, cudaStream_t s,
+                    unsigned flags) {
+    const I *inds = static_cast<const I *>(inds_);
+    const T *as = static_cast<const T *>(as_);
+    const T *hsb = static_cast<const T *>(hsb_);
+    T *ab = static_cast<T *>(ab_);
+    T *hs = static_cast<T *>(hs_);
+    const int acc = (flags & VJP_ACCUMULATE) ? 1 : 0;
+    const WideGeo g = wide_geo(n, m, w);
+    const int grid = grid_wide(g);
+    const int64_t mw = m * w;
+    if (op == VJP_ADD) {
+        if (hs) {
+            if (cudaMemsetAsync(hs, 0, sizeof(T) * (size_t)mw, s) != cudaSuccess) return VJP_ECUDA;
+            rbiw_add_hist<T, I><<<grid, kBThreads, 0, s>>>(inds, as, hs, g);
+            vjph::count_launch();
+        }
+        rbiw_add_bwd<T, I><<<grid, kBThreads, 0, s>>>(inds, hsb, ab, g, acc);
+        vjph::count_launch();
+        if (winners && cudaMemsetAsync(winners, 0xff, sizeof(int64_t) * (size_t)mw, s) != cudaSuccess) return VJP_ECUDA;
+        return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+    }
+    RbiParams P = params(n, mw, 0, ws, flags, 0, false);
+    const int gm = grid_for(mw, 4);
+    if (op == VJP_MUL) {
+        P.log_domain = 1;
+        rbi_init<VJP_MUL><<<gm, kBThreads, 0, s>>>(P);
+        rbiw_mul_fwd<T, I><<<grid, kBThreads, 0, s>>>(inds, as, P, g);
+        rbi_log_finalize<<<gm, kBThreads, 0, s>>>(P);
+        BLayout L = blayout(mw);
+        MulPack<T> *pk = reinterpret_cast<MulPack<T> *>(static_cast<unsigned char *>(ws) + L.pk);
+        rbi_mul_prep<T><<<gm, kBThreads, 0, s>>>(hsb, P.p, P.z, pk, mw, hs, winners);
+        rbiw_mul_bwd<T, I><<<grid, kBThreads, 0, s>>>(inds, as, pk, ab, g, acc);
+        vjph::count_launch(5);
+        return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+    }
+    if (!acc && cudaMemsetAsync(ab, 0, sizeof(T) * (size_t)(n * w), s) != cudaSuccess) return VJP_ECUDA;
+    if (op == VJP_MIN) {
+        rbi_init<VJP_MIN><<<gm, kBThreads, 0, s>>>(P);
+        rbiw_ext_a<T, I, VJP_MIN><<<grid, kBThreads, 0, s>>>(inds, as, P, g);
+        rbiw_ext_b<T, I, VJP_MIN><<<grid, kBThreads, 0, s>>>(inds, as, P, g);
+        rbiw_ext_scatter<T, VJP_MIN><<<gm, kBThreads, 0, s>>>(P.win, hsb, ab, g, acc, hs, winners);
+    } else {
+        rbi_init<VJP_MAX><<<gm, kBThreads, 0, s>>>(P);
+        rbiw_ext_a<T, I, VJP_MAX><<<grid, kBThreads, 0, s>>>(inds, as, P, g);
+        rbiw_ext_b<T, I, VJP_MAX><<<grid, kBThreads, 0, s>>>(inds, as, P, g);
+        rbiw_ext_scatter<T, VJP_MAX><<<gm, kBThreads, 0, s>>>(P.win, hsb, ab, g, acc, hs, winners);
+    }
+    vjph::count_launch(4);
+    return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+}
+
 vjp_status common_check(vjp_op op, vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, const void *inds,
                         const void *as, const void *hs_bar) {
     if (op == VJP_LINREC || op == VJP_MAT2) return VJP_EUNSUPPORTED;  // no rule in the paper
@@ -850,26 +1098,28 @@ vjp_status vjp_debug_log2_abs(const double *x, double *y, int64_t n, vjp_stream_
 }
 
 
-size_t vjp_reduce_by_index_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_t n, int64_t m) {
+size_t vjp_reduce_by_index_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_t n, int64_t m, int64_t width) {
     (void)dtype;
-    (void)n;
-    if (!op_ok(op) || m < 1 || n < 0) return 0;
+    if (!op_ok(op) || m < 1 || n < 0 || width < 1) return 0;
     if (op == VJP_ADD) return 0;
+    if (width > 1) return blayout(m * width, 0, false).total;
     return blayout(m, n, op != VJP_MUL).total;
 }
 
-vjp_status vjp_reduce_by_index(vjp_op op, vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, const void *inds,
-                               const void *as, const void *hs_bar, void *as_bar, void *hs, int64_t *winners, void *ws,
-                               size_t ws_bytes, vjp_stream_t stream, unsigned flags) {
+vjp_status vjp_reduce_by_index(vjp_op op, vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, int64_t width,
+                               const void *inds, const void *as, const void *hs_bar, void *as_bar, void *hs,
+                               int64_t *winners, void *ws, size_t ws_bytes, vjp_stream_t stream, unsigned flags) {
+    if (width < 1) return VJP_EINVAL;
     vjp_status st = common_check(op, dtype, itype, n, m, inds, as, hs_bar);
     if (st != VJP_OK || n == 0) return st;
     if (!as_bar) return VJP_EINVAL;
     if (!vjph::aligned16(as_bar)) return VJP_EALIGN;
     if (op == VJP_ADD && hs && !as) return VJP_EINVAL;  // the primal sum needs `as`
-    const size_t need = vjp_reduce_by_index_workspace_bytes(op, dtype, n, m);
+    const size_t need = vjp_reduce_by_index_workspace_bytes(op, dtype, n, m, width);
     if (ws_bytes < need || (need && !ws)) return VJP_EWORKSPACE;
     if (ws && !vjph::aligned16(ws)) return VJP_EALIGN;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (width > 1) return RBI_DISPATCH(run_wide, op, n, m, width, inds, as, hs_bar, as_bar, hs, winners, ws, s, flags);
     return RBI_DISPATCH(run_full, op, n, m, inds, as, hs_bar, as_bar, hs, winners, ws, s, flags);
 }
 
@@ -915,7 +1165,7 @@ vjp_status vjp_reduce_by_index_finish(vjp_op op, vjp_dtype dtype, vjp_itype ityp
     if (!as_bar) return VJP_EINVAL;
     if (!vjph::aligned16(as_bar)) return VJP_EALIGN;
     if (op != VJP_ADD && (!bin_val || !bin_aux)) return VJP_EINVAL;
-    const size_t need = vjp_reduce_by_index_workspace_bytes(op, dtype, n, m);
+    const size_t need = vjp_reduce_by_index_workspace_bytes(op, dtype, n, m, 1);
     if (ws_bytes < need || (need && !ws)) return VJP_EWORKSPACE;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     return RBI_DISPATCH(run_finish, op, n, m, shard->global_offset, inds, as, hs_bar, as_bar, bin_val, bin_aux, ws,

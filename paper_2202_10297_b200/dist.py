@@ -11,7 +11,8 @@ exchange step:
                   aggregates built with the forward carry: partial2).
   reduce          partial record (p, z, i0) / (value, index) / sum -> all_gather
                   -> finish (deterministic rank-order combine on the device).
-  reduce_by_index per-bin state -> all_reduce (PRODUCT+SUM for *, MAX/MIN then
+  reduce_by_index per-bin state -> all_reduce (integer SUM of the 64-bit factor
+                  codes and of the zero counts for *, MAX/MIN then
                   MIN of candidate indices for max/min) -> finish; ADD needs no
                   exchange (hs_bar is replicated).
   scatter         ys_bar partitioned, targets replicated: each rank zeroes its
@@ -153,14 +154,15 @@ def reduce_by_index(op, inds: torch.Tensor, as_: torch.Tensor | None, hs_bar: to
     s = _stream(dev)
     bin_val = torch.empty(m, dtype=torch.float64, device=dev)
     bin_aux = torch.empty(m, dtype=torch.int64, device=dev)
-    ws = workspace(L.vjp_reduce_by_index_workspace_bytes(o, dt, n, m), dev)
+    ws = workspace(L.vjp_reduce_by_index_workspace_bytes(o, dt, n, m, 1), dev)
     nbytes = 0 if ws is None else ws.numel()
     if o != 1:  # ADD needs no exchange: hs_bar is replicated
         _check(L.vjp_reduce_by_index_partial(o, dt, it, n, m, _p(inds), _p(as_), _p(ws), nbytes, sh, _p(bin_val),
                                              _p(bin_aux), s), "vjp_reduce_by_index_partial")
         if sh.world > 1:
-            if o == 2:  # MUL
-                _all_reduce(bin_val, dist.ReduceOp.PRODUCT, group)
+            if o == 2:  # MUL: the bins' 64-bit code sums (log2|a| fixed point + sign, mod 2^64) and zero counts
+                codes = bin_val.view(torch.int64)
+                _all_reduce(codes, dist.ReduceOp.SUM, group)
                 _all_reduce(bin_aux, dist.ReduceOp.SUM, group)
             else:
                 local = bin_val.clone()

@@ -341,3 +341,25 @@ def kmeans_inputs(n, k, d, *, dtype=torch.float64, offset=0, device="cpu", k_tru
     cnoise = _normal40(k * d, 630, device=device).reshape(k, d)
     centers = centres[torch.arange(k, device=device) % kt] + 0.1 * cnoise
     return points.to(dtype).contiguous(), centers.to(dtype).contiguous()
+
+def rbi_wide_inputs(n, m, width, op, *, dtype=torch.float64, itype=torch.int32, device="cpu"):
+    """reduce_by_index with a vectorised operator (rows of `width` components,
+    P:1229-1231): bins i.i.d. uniform over m; values [n x width] by the config-4
+    recipe per component ('*': log-centred 1 + (u-1/2)2^-10 with zeros of
+    probability ~ m/n; max/min: a 2^-12 grid for ties; '+': U(0,1));
+    hs_bar [m x width] ~ U(0.5, 1.5)."""
+    inds = integers(n, 410, 0, m - 1, device=device, dtype=itype)
+    nw = n * width
+    if op == "mul":
+        u = uniform(nw, 411, device=device)
+        a = (1.0 + (u - 0.5) * (2.0 ** -10)).to(dtype)
+        thr = int(min(1.0, m / max(n, 1)) * (1 << 62))
+        b = _srl(bits(nw, 412, device=device), 2)
+        a[b < thr] = 0.0
+    elif op in ("max", "min"):
+        k = integers(nw, 413, 0, (1 << 12) - 1, device=device)
+        a = (k.to(torch.float64) * (2.0 ** -12)).to(dtype)
+    else:
+        a = uniform(nw, 411, dtype=dtype, device=device)
+    hs_bar = uniform(m * width, 414, lo=0.5, hi=1.5, dtype=dtype, device=device)
+    return inds, a, hs_bar

@@ -155,8 +155,9 @@ def test_reduce_split_emulated(op, zeros, world):
 @pytest.mark.parametrize("op,m", [("add", 1000), ("mul", 1000), ("mul", 100_000), ("max", 1000),
                                   ("max", 100_000), ("min", 5000)])
 def test_rbi_split_emulated(op, m, world):
-    """per-bin state all-reduced (PRODUCT+SUM for *, MAX/MIN then MIN of the
-    candidate indices for max/min), then the finish per shard."""
+    """per-bin state all-reduced (integer SUM of the 64-bit factor codes and of
+    the zero counts for *, MAX/MIN then MIN of the candidate indices for
+    max/min), then the finish per shard."""
     L = vjp.lib()
     o = vjp.OPS[op]
     N = 400_009
@@ -167,7 +168,7 @@ def test_rbi_split_emulated(op, m, world):
     for r, (off, n) in enumerate(shards(N, world)):
         i_r = inds[off:off + n].clone().to(DEV)
         a_r = a[off:off + n].clone().to(DEV)
-        ws_n = L.vjp_reduce_by_index_workspace_bytes(o, 2, n, m)
+        ws_n = L.vjp_reduce_by_index_workspace_bytes(o, 2, n, m, 1)
         ws = torch.empty(max(ws_n, 1), dtype=torch.uint8, device=DEV)
         bv = torch.empty(m, dtype=torch.float64, device=DEV)
         ba = torch.empty(m, dtype=torch.int64, device=DEV)
@@ -178,7 +179,8 @@ def test_rbi_split_emulated(op, m, world):
         auxs.append(ba)
         state.append((i_r, a_r, ws, ws_n, sh, n))
     if op == "mul":
-        gv = torch.stack(vals).prod(0)
+        # codes add mod 2^64 (int64 two's complement wrap-around, as NCCL's SUM)
+        gv = torch.stack([v.view(torch.int64) for v in vals]).sum(0).view(torch.float64)
         ga = torch.stack(auxs).sum(0)
         gvs, gas = [gv] * world, [ga] * world
     elif op in ("max", "min"):

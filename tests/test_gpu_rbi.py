@@ -155,3 +155,60 @@ def test_rbi_mul_general_accumulate_and_unsupported():
     with pytest.raises(vjp.VjpError) as e:
         vjp.reduce_by_index("add", inds.to(DEV), a.to(DEV), hb.to(DEV), general=True)
     assert e.value.code == 2
+
+
+# ---------------------------------------------------------------- width > 1
+@pytest.mark.parametrize("dt", [np.float64, np.float32], ids=["f64", "f32"])
+@pytest.mark.parametrize("op", ["add", "mul", "min", "max"])
+@pytest.mark.parametrize("width", [2, 3, 8, 33, 64])
+def test_rbi_width(op, width, dt):
+    """vectorised operator (reading A24): per-(bin, component)
+    winners / zero counts bit-exact, adjoints vs the oracle (run per component)."""
+    n, m = 20_011, 300
+    inds, a, hb = synth.rbi_wide_inputs(n, m, width, op, dtype=TD[dt])
+    inds[1] = -1
+    inds[3] = m + 5
+    ref_ab, ref_hs, ref_win, ref_z = oracle.vjp_reduce_by_index(op, inds.numpy(), a.numpy(), hb.numpy(), width=width)
+    ab, hs, win = vjp.reduce_by_index(op, inds.to(DEV), a.to(DEV), hb.to(DEV), want_hs=True, width=width)
+    ab = ab.cpu().numpy()
+    if op in ("min", "max"):
+        assert np.array_equal(win.cpu().numpy(), ref_win), "winner indices differ"
+        assert np.array_equal(ab, ref_ab)
+    elif op == "mul":
+        assert np.array_equal(win.cpu().numpy(), ref_z), "zero counts differ"
+        assert_close(ab, ref_ab, dt, what=f"rbi mul width={width}")
+    else:
+        assert np.array_equal(ab, ref_ab)
+        assert_close(hs.cpu().numpy(), ref_hs, dt, scale=np.full(m * width, max(1.0, n / m)), what="primal sum")
+    # accumulate: only the documented elements change
+    base = synth.uniform(n * width, 700, dtype=TD[dt])
+    got = vjp.reduce_by_index(op, inds.to(DEV), a.to(DEV), hb.to(DEV), width=width, out=base.to(DEV),
+                              accumulate=True).cpu().numpy()
+    ref = oracle.vjp_reduce_by_index(op, inds.numpy(), a.numpy(), hb.numpy(), width=width,
+                                     out=base.numpy().copy(), accumulate=True)[0]
+    if op == "mul":
+        assert_close(got, ref, dt, what="rbi mul width accumulate")
+    else:
+        assert np.array_equal(got, ref)
+
+
+def test_rbi_width_goldens():
+    import json, os
+    cases = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))["cases"]
+    for c in cases:
+        if c["kind"] != "reduce_by_index" or c.get("width", 1) == 1:
+            continue
+        w = c["width"]
+        ab, hs, win = vjp.reduce_by_index(c["op"], torch.tensor(c["inds"], dtype=torch.int32, device=DEV),
+                                          torch.tensor(c["as"], dtype=torch.float64, device=DEV),
+                                          torch.tensor(c["hs_bar"], dtype=torch.float64, device=DEV),
+                                          want_hs=True, width=w)
+        if c["op"] == "mul":
+            assert_close(ab.cpu().numpy(), np.array(c["expected"], np.float64), np.float64, what=c["id"])
+            assert win.cpu().tolist() == c["zeros"]
+        else:
+            assert ab.cpu().tolist() == c["expected"], c["id"]
+        if "winners" in c:
+            assert win.cpu().tolist() == c["winners"], c["id"]
+        if "hs" in c:
+            assert hs.cpu().tolist() == c["hs"], c["id"]

@@ -56,7 +56,8 @@ def test_golden(case, dt):
         assert zeros == case["zeros"]
     elif k == "reduce_by_index":
         ab, hs, win, zeros = oracle.vjp_reduce_by_index(
-            case["op"], np.array(case["inds"], np.int32), _arr(case["as"], dt), _arr(case["hs_bar"], dt))
+            case["op"], np.array(case["inds"], np.int32), _arr(case["as"], dt), _arr(case["hs_bar"], dt),
+            width=case.get("width", 1))
         assert ab.tolist() == _arr(case["expected"], dt).tolist()
         if "hs" in case:
             assert hs.tolist() == _arr(case["hs"], dt).tolist()
