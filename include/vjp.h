@@ -47,6 +47,10 @@
  *  - Arithmetic: f64 data is computed in f64; f32 data is loaded as f32 and
  *    computed/accumulated in f64, outputs rounded once to f32 (reading R9).
  *    Round-to-nearest-even, no flush-to-zero.
+ *  - A call's behaviour depends only on its arguments.  Tuning environment
+ *    variables (VJP_SWEEP_K / _D / _ROUND_MB, VJP_LB_L2_MB, VJP_LB_VARIANT,
+ *    VJP_KMEANS_FFMA; testing only) are read ONCE per process at first use,
+ *    never per call.
  */
 #ifndef VJP_B200_H
 #define VJP_B200_H
@@ -98,8 +102,8 @@ enum {
                                     default for f64 ADD without ys */
     VJP_SCAN_CHUNKED = 1u << 18,  /* tuning/testing: force the two chunked kernels */
     VJP_SCAN_BLOCKLB = 1u << 19   /* tuning/testing: force the one-read block look-back
-                                    (single GPU; the default for every operator except f64
-                                    scan(+) without ys) */
+                                    (single GPU, no ACCUMULATE; opt-in: measured slower than
+                                    the chunked kernels) */
 };
 
 /* One shard of a multi-GPU call: this process owns global elements
@@ -158,9 +162,10 @@ vjp_status vjp_scan(vjp_op op, vjp_dtype dtype, int64_t n, const void *as,
  *      forward carry (ranks < rank) and reverse carry (ranks > rank) combined
  *      from `gathered` on the device.
  * `n` is the LOCAL element count; `ws` must be the same workspace for both
- * phases (the finish reads the partial's per-tile prefixes).  MIN/MAX return
- * VJP_EUNSUPPORTED for world > 1 (their reverse coefficients depend on the
- * forward carry).  vjp_scan == partial + finish with world = 1. */
+ * phases (the finish reads the partial's per-tile prefixes).  MIN/MAX need a
+ * second exchange (their reverse coefficients depend on the forward carry):
+ * vjp_scan_partial2 below.  vjp_scan == partial + finish with world = 1.
+ * An empty shard (n == 0) writes the neutral record. */
 size_t vjp_scan_partial_bytes(vjp_op op, vjp_dtype dtype);
 vjp_status vjp_scan_partial(vjp_op op, vjp_dtype dtype, int64_t n, const void *as,
                             const void *ys_bar, void *ws, size_t ws_bytes,
@@ -179,6 +184,71 @@ vjp_status vjp_scan_partial2(vjp_op op, vjp_dtype dtype, int64_t n, const void *
 vjp_status vjp_scan_finish(vjp_op op, vjp_dtype dtype, int64_t n, const void *as,
                            const void *ys_bar, void *as_bar, void *ys, void *ws,
                            size_t ws_bytes, const vjp_shard *shard, const void *gathered,
+                           vjp_stream_t stream, unsigned flags);
+
+/* ======================================================================
+ * vjp_scan_cyclic — BLOCK-CYCLIC multi-GPU vjp_scan with a cross-GPU
+ * decoupled look-back (the return sweep is a
+ * scan with the associative lin_o, so its superblock aggregates compose).
+ *
+ * The global array of global_n elements is cut into superblocks (SB) of
+ * sb_elems elements (the last one ragged).  SB J belongs to rank J % world;
+ * a rank's LOCAL arrays (as, ys_bar, as_bar) hold its SBs J = rank, rank +
+ * world, ... concatenated in increasing J (vjp_scan_cyclic_local_n elements).
+ * Every rank runs ONE persistent sweep over its SBs from right to left, one
+ * SB per round: all CTAs stream the SB once from HBM (the method bytes — no
+ * pre-pass over ys_bar, unlike the contiguous split), compose the SB's
+ * reverse map M_J, and CTA 0 pushes it (AGG) into EVERY rank's status buffer
+ * over NVLink (peer-mapped stores, sys-scope release), looks back over the
+ * status words of SBs J+1, J+2, ... (pushed by the other ranks) until an
+ * INCL carry is found, and pushes E_J = M_J(X_J) (INCL); the CTAs then apply
+ * the SB from L2 with the carry X_J.  No collective call on the ys_bar path.
+ * For MUL / LINREC / MAT2 the forward re-execution needs each SB's forward
+ * prefix: vjp_scan_cyclic_forward writes this rank's per-SB forward
+ * aggregates (reads `as` once), the caller all-gathers them (world x
+ * vjp_scan_cyclic_fwd_bytes, rank order) and passes the result as
+ * `gathered` (ADD: neither call nor gathered is needed).
+ *
+ *   status[q]  rank q's status buffer (vjp_scan_cyclic_status_bytes), mapped
+ *              into this process (torch symmetric memory / cudaIpc); zeroed
+ *              once at allocation.  Word 0 of a rank's own buffer is set
+ *              non-zero if one of its look-back waits timed out (a missing
+ *              peer): the results of that call are then invalid.  Words
+ *              1..8 hold the epoch each rank entered last: a call's first
+ *              status write waits until every rank owning a superblock has
+ *              entered its epoch (an in-kernel entry barrier, so one rank
+ *              can never overwrite words another is still reading).
+ *   epoch      1 .. 2^30-1, equal on all ranks for one call and STRICTLY
+ *              INCREASING from call to call on the same status buffers (the
+ *              status words carry it, so they are never reset).
+ *   grid_ctas  0: the whole device, one cooperatively launched wave; > 0:
+ *              that many CTAs (several virtual ranks sharing one device in
+ *              tests — the caller keeps all ranks' CTAs co-resident).
+ * All ranks must run the call concurrently (a rank's sweep waits on its
+ * right neighbours' superblocks).  Errors: VJP_EINVAL (descriptor, sizes,
+ * sb_elems not a multiple of vjp_scan_cyclic_tile_elems, or too large for
+ * the grid: more than 8 tiles per CTA), VJP_EUNSUPPORTED (MIN/MAX: their
+ * reverse maps need the forward carry), VJP_EWORKSPACE (vjp_scan_workspace_
+ * bytes(op, dtype, n_local)), VJP_ECUDA.  Flags: VJP_ACCUMULATE.
+ * ==================================================================== */
+#define VJP_CYCLIC_MAX_RANKS 8
+typedef struct {
+    int32_t rank, world;
+    int64_t global_n;   /* elements of the whole problem */
+    int64_t sb_elems;   /* superblock elements (same on every rank) */
+    uint32_t epoch;
+    int32_t grid_ctas;
+    void *status[VJP_CYCLIC_MAX_RANKS];  /* [world] peer-mapped DEVICE pointers */
+} vjp_cyclic;
+int64_t vjp_scan_cyclic_tile_elems(vjp_op op, vjp_dtype dtype);
+int64_t vjp_scan_cyclic_sb_elems(vjp_op op, vjp_dtype dtype); /* suggested SB size for this device */
+int64_t vjp_scan_cyclic_local_n(const vjp_cyclic *cy);
+size_t vjp_scan_cyclic_status_bytes(vjp_op op, int64_t global_n, int64_t sb_elems);
+size_t vjp_scan_cyclic_fwd_bytes(vjp_op op, vjp_dtype dtype, const vjp_cyclic *cy);
+vjp_status vjp_scan_cyclic_forward(vjp_op op, vjp_dtype dtype, int64_t n_local, const void *as, void *ws,
+                                   size_t ws_bytes, const vjp_cyclic *cy, void *sbagg, vjp_stream_t stream);
+vjp_status vjp_scan_cyclic(vjp_op op, vjp_dtype dtype, int64_t n_local, const void *as, const void *ys_bar,
+                           void *as_bar, void *ws, size_t ws_bytes, const vjp_cyclic *cy, const void *gathered,
                            vjp_stream_t stream, unsigned flags);
 
 /* Host-side (CPU, no device) evaluation of the carry combination that
@@ -208,7 +278,12 @@ vjp_status vjp_scan_carries_host(vjp_op op, vjp_dtype dtype, int32_t rank, int32
  *   as_bar [n] output.
  *   y      nullable DEVICE [1]: primal result (MUL: 0 if z > 0, else p).
  *   arg    nullable DEVICE int64[1]: i_y (MIN/MAX), i0 or -1 (MUL), -1 (ADD).
- * Errors: VJP_EINVAL (LINREC/MAT2 tags), VJP_EALIGN, VJP_EWORKSPACE, VJP_ECUDA.
+ *   LINREC / MAT2 : the paper's GENERAL reduce rule: y_bar is
+ *         one element (W scalars) and as_bar_i = J_R^T (l_i, a_i) applied to
+ *         the reverse product of the elements right of i — computed as the
+ *         scan's return sweep seeded only at the last element (scan-last ==
+ *         reduce) with a virtual ys_bar; y (nullable) = the reduction.
+ * Errors: VJP_EINVAL, VJP_EALIGN, VJP_EWORKSPACE, VJP_ECUDA.
  * ==================================================================== */
 size_t vjp_reduce_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_t n);
 vjp_status vjp_reduce(vjp_op op, vjp_dtype dtype, int64_t n, const void *as,
@@ -381,9 +456,10 @@ vjp_status vjp_scatter_forward(vjp_dtype dtype, vjp_itype itype, int64_t n, int6
 vjp_status vjp_scatter_restore(vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, int64_t width,
                                const void *is, const void *xs_saved, void *ys, vjp_stream_t stream);
 
-/* Test hook: y[i] = log2|x[i]| (DEVICE arrays, f64) by the routine the MUL
- * histograms accumulate with (reduce_by_index log domain). */
-vjp_status vjp_debug_log2_abs(const double *x, double *y, int64_t n, vjp_stream_t stream);
+/* Test hook: code[i] = the 64-bit factor code the MUL histograms accumulate
+ * (reduce_by_index, DESIGN 7.4): round(log2|x[i]| 2^51) + [x[i] < 0] 2^63
+ * mod 2^64, as computed by the kernels (x finite, nonzero; DEVICE arrays). */
+vjp_status vjp_debug_mul_code(const double *x, int64_t *code, int64_t n, vjp_stream_t stream);
 
 /* ======================================================================
  * vjp_scan_batched — vjp of a VECTORISED scan

@@ -49,6 +49,16 @@ class VjpShard(ctypes.Structure):
                 ("global_n", ctypes.c_int64)]
 
 
+CYCLIC_MAX_RANKS = 8
+
+
+class VjpCyclic(ctypes.Structure):
+    """vjp_cyclic (include/vjp.h): block-cyclic multi-GPU scan descriptor."""
+    _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("global_n", ctypes.c_int64),
+                ("sb_elems", ctypes.c_int64), ("epoch", ctypes.c_uint32), ("grid_ctas", ctypes.c_int32),
+                ("status", ctypes.c_void_p * CYCLIC_MAX_RANKS)]
+
+
 def lib():
     """Load libvjp_b200.so (raises if it was not built: no fallback)."""
     global _lib
@@ -59,6 +69,7 @@ def lib():
         L = ctypes.CDLL(LIB_PATH)
         vp, i64, sz, u32, ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_size_t, ctypes.c_uint, ctypes.c_int
         sp = ctypes.POINTER(VjpShard)
+        cy = ctypes.POINTER(VjpCyclic)
         sig = {
             "vjp_status_string": ([ci], ctypes.c_char_p),
             "vjp_launch_count": ([], ctypes.c_uint64),
@@ -88,9 +99,16 @@ def lib():
             "vjp_scatter_restore": ([ci, ci, i64, i64, i64, vp, vp, vp, vp], ci),
             "vjp_kmeans_workspace_bytes": ([ci, i64, i64, i64], sz),
             "vjp_scan_batched_workspace_bytes": ([ci, ci, i64, i64], sz),
-            "vjp_debug_log2_abs": ([vp, vp, i64, vp], ci),
+            "vjp_debug_mul_code": ([vp, vp, i64, vp], ci),
             "vjp_scan_batched": ([ci, ci, i64, i64, vp, vp, vp, vp, sz, vp, u32], ci),
             "vjp_kmeans": ([ci, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, u32], ci),
+            "vjp_scan_cyclic_tile_elems": ([ci, ci], i64),
+            "vjp_scan_cyclic_sb_elems": ([ci, ci], i64),
+            "vjp_scan_cyclic_local_n": ([cy], i64),
+            "vjp_scan_cyclic_status_bytes": ([ci, i64, i64], sz),
+            "vjp_scan_cyclic_fwd_bytes": ([ci, ci, cy], sz),
+            "vjp_scan_cyclic_forward": ([ci, ci, i64, vp, vp, sz, cy, vp, vp], ci),
+            "vjp_scan_cyclic": ([ci, ci, i64, vp, vp, vp, vp, sz, cy, vp, vp, u32], ci),
         }
         for name, (args, res) in sig.items():
             if not hasattr(L, name):

@@ -21,6 +21,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "log2_table.cuh"
 
 namespace vjpk {
 
@@ -218,60 +219,6 @@ __device__ __forceinline__ void rbi_stream(const I *__restrict__ inds, const T *
     }
 }
 
-// log2|x| = e + l for finite x != 0 (the MUL histograms' log domain), without
-// the library routine's special-case paths: x = m * 2^e with m in [sqrt(1/2),
-// sqrt(2)), l = log2 m = (2/ln 2) atanh(s), s = (m - 1)/(m + 1) (|s| <= 0.1716;
-// m - 1 is exact by Sterbenz), atanh(s)/s = sum_k s^(2k)/(2k+1) to k = 11
-// (truncation < 1e-18).  |l| <= 1/2, error a few ulp of l (measured against
-// log2() in tests/test_gpu_rbi.py::test_rbi_mul_log2_accuracy).  Denormals are
-// rescaled.
-__device__ __forceinline__ double log2_split(double x, int &e_out) {
-    long long b = __double_as_longlong(x) & 0x7fffffffffffffffll;
-    int e = (int)(b >> 52);
-    if (e == 0) {  // subnormal
-        b = __double_as_longlong(__longlong_as_double(b) * 0x1p54);
-        e = (int)(b >> 52) - 54;
-    }
-    e -= 1023;
-    double m = __longlong_as_double((b & 0x000fffffffffffffll) | 0x3ff0000000000000ll);
-    if (m > 1.4142135623730951) {
-        m *= 0.5;
-        e += 1;
-    }
-    // s = (m - 1) / (m + 1) without the IEEE division's special-case path
-    // (m + 1 in [1.7, 2.5): normal, no overflow): hardware reciprocal
-    // estimate, two Newton steps, one residual correction of the quotient
-    const double num = m - 1.0, den = m + 1.0;
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(den));
-    r = fma(r, fma(-den, r, 1.0), r);
-    r = fma(r, fma(-den, r, 1.0), r);
-    double s = num * r;
-    s = fma(r, fma(-s, den, num), s);
-    const double s2 = s * s;
-    double p = 1.0 / 23.0;
-    p = fma(p, s2, 1.0 / 21.0);
-    p = fma(p, s2, 1.0 / 19.0);
-    p = fma(p, s2, 1.0 / 17.0);
-    p = fma(p, s2, 1.0 / 15.0);
-    p = fma(p, s2, 1.0 / 13.0);
-    p = fma(p, s2, 1.0 / 11.0);
-    p = fma(p, s2, 1.0 / 9.0);
-    p = fma(p, s2, 1.0 / 7.0);
-    p = fma(p, s2, 1.0 / 5.0);
-    p = fma(p, s2, 1.0 / 3.0);
-    const double t = s * s2 * p;  // atanh(s) - s
-    // log2 m = 2 (s + t) / ln 2, with 2/ln 2 split hi + lo for the dominant term
-    const double k_hi = 2.8853900817779268, k_lo = 4.0710547481862066e-17;
-    e_out = e;
-    return fma(s, k_hi, fma(s, k_lo, t * k_hi));
-}
-__device__ __forceinline__ double log2_abs(double x) {
-    int e;
-    const double l = log2_split(x, e);
-    return (double)e + l;
-}
-
 // The MUL histograms accumulate, per bin, ONE 64-bit integer code per
 // nonzero factor a (reading R13b, DESIGN 7.4):
 //     code(a) = round(log2|a| * 2^51)  +  (a < 0 ? 2^63 : 0)      (mod 2^64)
@@ -283,10 +230,48 @@ __device__ __forceinline__ double log2_abs(double x) {
 // parity = bit 63 of (T - L); p = (-1)^parity * 2^(L / 2^51).  Quantisation
 // error 2^-52 per factor on log2, i.e. <= 0.7 * 2^-52 * n_b relative on p
 // (n_b = factors in the bin): 4e-11 at n_b = 2.7e5 (config 4, m = 10^3).
-__device__ __forceinline__ unsigned long long mul_code(double x) {
-    int e;
-    const double l = log2_split(x, e);  // |l| <= 1/2: l * 2^51 exact in f64
-    const long long q = ((long long)e << 51) + __double2ll_rn(l * 0x1p51);
+// The code's log2 by table + short series (no division, ~13 FP64 ops): x =
+// m * 2^e, m in [1, 2); k = top 7 bits of m's fraction; inv_k ~ 1/c_k and
+// T_k = -log2(inv_k) exactly (hi + lo) from log2_table.cuh (staged in shared
+// memory: divergent lookups); m * inv_k = 1 + r, |r| < 2^-7.9, r from one FMA
+// (error <= 2^-61); log2(1 + r) = (r + r^2 P(r)) / ln 2, P the ln(1+r)
+// series to r^6 (truncation < 2^-58); the products by 1/ln 2 carry an error
+// term, so the code is within ~2^-52 of log2|x| * 2^51 rounded.
+struct Log2Tab {
+    double inv[128], hi[128], lo[128];
+};
+__device__ __forceinline__ void log2tab_load(Log2Tab &t) {
+    for (int k = threadIdx.x; k < 128; k += blockDim.x) {
+        t.inv[k] = kLog2Tab[k][0];
+        t.hi[k] = kLog2Tab[k][1];
+        t.lo[k] = kLog2Tab[k][2];
+    }
+}
+__device__ __constant__ double kLn1pP[5] = {-1.0 / 6.0, 1.0 / 5.0, -1.0 / 4.0, 1.0 / 3.0, -1.0 / 2.0};
+__device__ __forceinline__ unsigned long long mul_code(double x, const Log2Tab &tb) {
+    long long b = __double_as_longlong(x) & 0x7fffffffffffffffll;
+    int e = (int)(b >> 52);
+    if (e == 0) {  // subnormal
+        b = __double_as_longlong(__longlong_as_double(b) * 0x1p54);
+        e = (int)(b >> 52) - 54;
+    }
+    e -= 1023;
+    const int k = (int)((b >> 45) & 127);
+    const double m = __longlong_as_double((b & 0x000fffffffffffffll) | 0x3ff0000000000000ll);
+    const double r = fma(m, tb.inv[k], -1.0);
+    const double r2 = r * r;
+    double P = fma(kLn1pP[0], r, kLn1pP[1]);
+    P = fma(P, r, kLn1pP[2]);
+    P = fma(P, r, kLn1pP[3]);
+    P = fma(P, r, kLn1pP[4]);
+    const double u = r2 * P;  // ln(1 + r) = r + u
+    const double K_hi = 1.4426950408889634, K_lo = 2.0355273740931033e-17;  // 1 / ln 2
+    const double s_hi = r * K_hi;
+    double s_lo = fma(r, K_hi, -s_hi);
+    s_lo = fma(r, K_lo, s_lo);
+    s_lo = fma(u, K_hi, s_lo);
+    const double L = tb.hi[k] + (s_hi + (s_lo + tb.lo[k]));  // log2 m in [0, 1]
+    const long long q = ((long long)e << 51) + __double2ll_rn(L * 0x1p51);
     return (unsigned long long)q + (x < 0.0 ? 0x8000000000000000ull : 0ull);
 }
 __device__ __forceinline__ double mul_decode(unsigned long long T) {
@@ -299,10 +284,13 @@ __device__ __forceinline__ double mul_decode(unsigned long long T) {
     return neg ? -v : v;
 }
 
-// test hook: log2_abs on n values (tests compare it with log2 on the device)
-__global__ void rbi_log2_probe(const double *x, double *y, int64_t n) {
+// test hook: the factor codes of n values (tests compare them with exact codes)
+__global__ void rbi_code_probe(const double *x, unsigned long long *y, int64_t n) {
+    __shared__ Log2Tab tb;
+    log2tab_load(tb);
+    __syncthreads();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) y[i] = log2_abs(x[i]);
+    if (i < n) y[i] = mul_code(x[i], tb);
 }
 
 // MUL, large m: every element must contribute, and a CAS-multiply costs two
@@ -312,10 +300,13 @@ __global__ void rbi_log2_probe(const double *x, double *y, int64_t n) {
 template <class T, class I>
 __global__ void __launch_bounds__(kBThreads) rbi_fwd_log(const I *__restrict__ inds, const T *__restrict__ as,
                                                          RbiParams P) {
+    __shared__ Log2Tab tb;
+    log2tab_load(tb);
+    __syncthreads();
     rbi_stream<T, I>(inds, as, nullptr, P, [&](int64_t b, double x, int64_t, bool ok) {
         if (!ok) return;
         if (x == 0.0) atomicAdd(P.z + b, 1ull);
-        else atomicAdd(P.code + b, mul_code(x));
+        else atomicAdd(P.code + b, mul_code(x, tb));
     });
 }
 // small m: one shared-memory table per CTA.  Shared-memory atomics are native
@@ -329,22 +320,64 @@ template <class T, class I>
 __global__ void __launch_bounds__(kBThreads, kBMinBlocks) rbi_fwd_smem_log(const I *__restrict__ inds, const T *__restrict__ as,
                                                               RbiParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ Log2Tab tb;
+    log2tab_load(tb);
     unsigned *lo = reinterpret_cast<unsigned *>(smem);
     unsigned *hi = lo + P.m;
     unsigned *zc = hi + P.m;
     for (int64_t b = threadIdx.x; b < P.m; b += blockDim.x) { lo[b] = 0u; hi[b] = 0u; zc[b] = 0u; }
     __syncthreads();
-    rbi_stream<T, I>(inds, as, nullptr, P, [&](int64_t b, double x, int64_t, bool ok) {
-        if (!ok) return;
+    const uint64_t m = (uint64_t)P.m;
+    // 32-bit shared-window addresses, computed once (the generic-pointer
+    // atomics re-derived the window base for every element)
+    const uint32_t a_lo = smem_u32(lo), a_hi = smem_u32(hi), a_zc = smem_u32(zc);
+    auto visit = [&](int64_t b, double x) {
+        if ((uint64_t)b >= m) return;  // out-of-range bins (negative ones wrap): skipped (R4)
+        const uint32_t o = (uint32_t)b * 4u;
         if (x == 0.0) {
-            atomicAdd(zc + b, 1u);
+            asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(a_zc + o) : "memory");
         } else {
-            const unsigned long long q = mul_code(x);
+            const unsigned long long q = mul_code(x, tb);
             const unsigned ql = (unsigned)q;
-            const unsigned old = atomicAdd(lo + b, ql);
-            atomicAdd(hi + b, (unsigned)(q >> 32) + (old + ql < old ? 1u : 0u));
+            unsigned old;
+            asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a_lo + o), "r"(ql) : "memory");
+            const unsigned qh = (unsigned)(q >> 32) + (old + ql < old ? 1u : 0u);
+            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a_hi + o), "r"(qh) : "memory");
         }
-    });
+    };
+    // slab loop unrolled by two (ping-pong register buffers: no copies)
+    {
+        const int64_t ns = P.n / 128;
+        const int lane = threadIdx.x & 31;
+        const int64_t ws = ((int64_t)gridDim.x * blockDim.x) >> 5;
+        const uint64_t pol = policy_evict_first();
+        int64_t sl = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+        int64_t ba[4], bb[4];
+        double xa[4], xb[4];
+        if (sl < ns) {
+            ld_bins4(inds, sl * 128 + lane * 4, ba, pol);
+            ld_vals4(as, sl * 128 + lane * 4, xa, pol, P.v256);
+        }
+        for (; sl < ns; sl += 2 * ws) {
+            const int64_t s1 = sl + ws, s2 = sl + 2 * ws;
+            if (s1 < ns) {
+                ld_bins4(inds, s1 * 128 + lane * 4, bb, pol);
+                ld_vals4(as, s1 * 128 + lane * 4, xb, pol, P.v256);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) visit(ba[q], xa[q]);
+            if (s1 >= ns) break;
+            if (s2 < ns) {
+                ld_bins4(inds, s2 * 128 + lane * 4, ba, pol);
+                ld_vals4(as, s2 * 128 + lane * 4, xa, pol, P.v256);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) visit(bb[q], xb[q]);
+        }
+        if (blockIdx.x == 0 && threadIdx.x < 32) {  // tail (< 128 elements)
+            for (int64_t e = ns * 128 + lane; e < P.n; e += 32) visit((int64_t)inds[e], (double)as[e]);
+        }
+    }
     __syncthreads();
     for (int64_t b = threadIdx.x; b < P.m; b += blockDim.x) {
         const unsigned long long t = ((unsigned long long)hi[b] << 32) | lo[b];
@@ -684,6 +717,9 @@ __global__ void __launch_bounds__(kBThreads) rbiw_add_hist(const I *__restrict__
 template <class T, class I>
 __global__ void __launch_bounds__(kBThreads) rbiw_mul_fwd(const I *__restrict__ inds, const T *__restrict__ as,
                                                           RbiParams P, WideGeo g) {
+    __shared__ Log2Tab tb;
+    log2tab_load(tb);
+    __syncthreads();
     int64_t i, rs;
     int lane;
     wide_start(g, i, rs, lane);
@@ -693,7 +729,7 @@ __global__ void __launch_bounds__(kBThreads) rbiw_mul_fwd(const I *__restrict__ 
         for (int64_t j = lane; j < g.w; j += g.gw) {
             const double x = (double)__ldg(as + i * g.w + j);
             if (x == 0.0) atomicAdd(P.z + b * g.w + j, 1ull);
-            else atomicAdd(P.code + b * g.w + j, mul_code(x));
+            else atomicAdd(P.code + b * g.w + j, mul_code(x, tb));
         }
     }
 }
@@ -1088,11 +1124,12 @@ vjp_status common_check(vjp_op op, vjp_dtype dtype, vjp_itype itype, int64_t n, 
 
 extern "C" {
 
-// test hook for the MUL log domain: y[i] = log2|x[i]| by the kernels' routine
-vjp_status vjp_debug_log2_abs(const double *x, double *y, int64_t n, vjp_stream_t stream) {
-    if (n < 0 || (n > 0 && (!x || !y))) return VJP_EINVAL;
+// test hook for the MUL codes: code[i] = code(x[i]) by the kernels' routine
+vjp_status vjp_debug_mul_code(const double *x, int64_t *code, int64_t n, vjp_stream_t stream) {
+    if (n < 0 || (n > 0 && (!x || !code))) return VJP_EINVAL;
     if (n == 0) return VJP_OK;
-    vjpk::rbi_log2_probe<<<(unsigned)((n + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(x, y, n);
+    vjpk::rbi_code_probe<<<(unsigned)((n + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+        x, reinterpret_cast<unsigned long long *>(code), n);
     vjph::count_launch();
     return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
 }

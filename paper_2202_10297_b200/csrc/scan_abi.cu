@@ -216,6 +216,104 @@ vjp_status vjp_scan_carries_host(vjp_op op, vjp_dtype dtype, int32_t rank, int32
     return VJP_EINVAL;
 }
 
+// ---------------- block-cyclic multi-GPU vjp_scan ----------------
+// geometry of the descriptor (what the size queries need)
+static bool cyc_geo_ok(vjp_op op, vjp_dtype dtype, const vjp_cyclic *cy) {
+    if (!cy || !dtype_ok(dtype) || !disp_for(op)) return false;
+    if (cy->world < 1 || cy->world > VJP_CYCLIC_MAX_RANKS || cy->rank < 0 || cy->rank >= cy->world) return false;
+    if (cy->global_n < 0 || cy->sb_elems <= 0 || cy->grid_ctas < 0) return false;
+    const int64_t te = vjp_scan_cyclic_tile_elems(op, dtype);
+    return te > 0 && cy->sb_elems % te == 0;
+}
+// ... plus what a call needs
+static bool cyc_ok(vjp_op op, vjp_dtype dtype, const vjp_cyclic *cy) {
+    if (!cyc_geo_ok(op, dtype, cy)) return false;
+    if (cy->epoch == 0 || cy->epoch >= (1u << 30)) return false;
+    for (int q = 0; q < cy->world; ++q)
+        if (!cy->status[q] || !aligned16(cy->status[q])) return false;
+    return true;
+}
+
+int64_t vjp_scan_cyclic_tile_elems(vjp_op op, vjp_dtype dtype) {
+    if (!dtype_ok(dtype) || !disp_for(op)) return 0;
+    const int w = op == VJP_LINREC ? 2 : (op == VJP_MAT2 ? 4 : 1);
+    const int es = w * (dtype == VJP_F64 ? 8 : 4);
+    return (int64_t)(vjpk::kRowBytes / es) * 128;  // one 128-row TMA tile of the chunked / sweep kernels
+}
+
+int64_t vjp_scan_cyclic_sb_elems(vjp_op op, vjp_dtype dtype) {
+    Disp d = disp_for(op);
+    if (!d || !dtype_ok(dtype)) return 0;
+    ScanCall c{};
+    c.op = op;
+    c.dtype = dtype;
+    size_t out = 0;
+    if (d(kCycSbTiles, c, &out) != VJP_OK) return 0;
+    return (int64_t)out;
+}
+
+int64_t vjp_scan_cyclic_local_n(const vjp_cyclic *cy) {
+    if (!cy || cy->world < 1 || cy->rank < 0 || cy->rank >= cy->world || cy->sb_elems <= 0 || cy->global_n < 0)
+        return -1;
+    const int64_t nsb = (cy->global_n + cy->sb_elems - 1) / cy->sb_elems;
+    int64_t n = 0;
+    for (int64_t J = cy->rank; J < nsb; J += cy->world) {
+        const int64_t e = (J + 1) * cy->sb_elems < cy->global_n ? (J + 1) * cy->sb_elems : cy->global_n;
+        n += e - J * cy->sb_elems;
+    }
+    return n;
+}
+
+size_t vjp_scan_cyclic_status_bytes(vjp_op op, int64_t global_n, int64_t sb_elems) {
+    if (!disp_for(op) || global_n < 0 || sb_elems <= 0) return 0;
+    const int64_t nsb = (global_n + sb_elems - 1) / sb_elems;
+    const int w = op == VJP_LINREC ? 2 : (op == VJP_MAT2 ? 4 : 1);
+    const int md = op == VJP_MAT2 ? 8 : (op == VJP_LINREC ? 3 : (op == VJP_MUL ? 2 : 1));
+    return 256 + align256((size_t)nsb * 4) + align256((size_t)nsb * (md + w) * 8);
+}
+
+size_t vjp_scan_cyclic_fwd_bytes(vjp_op op, vjp_dtype dtype, const vjp_cyclic *cy) {
+    if (!cyc_geo_ok(op, dtype, cy)) return 0;
+    const int w = op == VJP_LINREC ? 2 : (op == VJP_MAT2 ? 4 : 1);
+    const int64_t nsb = (cy->global_n + cy->sb_elems - 1) / cy->sb_elems;
+    const int64_t nloc_max = nsb > 0 ? (nsb - 1) / cy->world + 1 : 0;
+    return (size_t)(nloc_max > 0 ? nloc_max : 1) * w * 8;
+}
+
+vjp_status vjp_scan_cyclic_forward(vjp_op op, vjp_dtype dtype, int64_t n_local, const void *as, void *ws,
+                                   size_t ws_bytes, const vjp_cyclic *cy, void *sbagg, vjp_stream_t stream) {
+    if (!cyc_ok(op, dtype, cy)) return VJP_EINVAL;
+    if (op == VJP_MIN || op == VJP_MAX) return VJP_EUNSUPPORTED;
+    if (n_local != vjp_scan_cyclic_local_n(cy)) return VJP_EINVAL;
+    if (op == VJP_ADD || n_local == 0) return VJP_OK;  // closed form / nothing owned: no forward pass
+    if (!as || !sbagg || !aligned16(as) || !aligned16(sbagg)) return VJP_EINVAL;
+    ScanCall c = make_call(op, dtype, n_local, as, as, nullptr, nullptr, ws, ws_bytes, stream, 0, nullptr);
+    c.cyc = cy;
+    c.partial = sbagg;
+    size_t need = 0;
+    disp_for(op)(kScanWs, c, &need);
+    if (ws_bytes < need || !ws || !aligned16(ws)) return VJP_EWORKSPACE;
+    return disp_for(op)(kCycForward, c, nullptr);
+}
+
+vjp_status vjp_scan_cyclic(vjp_op op, vjp_dtype dtype, int64_t n_local, const void *as, const void *ys_bar,
+                           void *as_bar, void *ws, size_t ws_bytes, const vjp_cyclic *cy, const void *gathered,
+                           vjp_stream_t stream, unsigned flags) {
+    if (!cyc_ok(op, dtype, cy)) return VJP_EINVAL;
+    if (op == VJP_MIN || op == VJP_MAX) return VJP_EUNSUPPORTED;
+    if (n_local != vjp_scan_cyclic_local_n(cy)) return VJP_EINVAL;
+    if (flags & ~(unsigned)VJP_ACCUMULATE) return VJP_EINVAL;
+    ScanCall c = make_call(op, dtype, n_local, as, ys_bar, as_bar, nullptr, ws, ws_bytes, stream, flags, nullptr);
+    c.cyc = cy;
+    c.gathered = gathered;
+    c.world = 1;  // the chunked shard logic is not used: the sweep's look-back does the exchange
+    if (n_local == 0) return VJP_OK;  // (a rank owning no superblock publishes nothing: no SB waits on it)
+    vjp_status s = check(c, true);
+    if (s != VJP_OK) return s;
+    if (op != VJP_ADD && (!gathered || !aligned16(gathered))) return VJP_EINVAL;
+    return disp_for(op)(kCycFinish, c, nullptr);
+}
+
 // tuning hook: per-block timestamps of the block look-back (DEVICE buffer of
 // 8 u64 per block, zeroed by the caller; nullptr turns it off)
 vjp_status vjp_debug_lb_trace(unsigned long long *buf) {

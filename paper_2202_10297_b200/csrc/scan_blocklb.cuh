@@ -82,11 +82,7 @@ struct LbSmem {
     double rm[Op::kMapD * RowArr<NT>::kStride];
 };
 
-__device__ __forceinline__ uint64_t globaltimer_ns() {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
+// (globaltimer_ns: scan_sweep.cuh)
 // barrier of the 4 compute warps only (the look-back warp never joins)
 __device__ __forceinline__ void csync() { asm volatile("bar.sync 1, %0;" ::"n"(kLbCompute) : "memory"); }
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }

@@ -52,10 +52,11 @@ struct ScanCall {
     int64_t global_offset;
     void *partial;         // partial phase: record output (device)
     const void *gathered;  // finish phase: world records (device)
+    const vjp_cyclic *cyc; // block-cyclic multi-GPU call (f1), else nullptr
 };
 
 enum ScanPhase { kScanWs = 0, kScanPartial = 1, kScanFinish = 2, kScanPartialBytes = 3, kReduceGeneral = 4,
-                 kScanPartial2 = 5, kScanIdentity = 6 };
+                 kScanPartial2 = 5, kScanIdentity = 6, kCycForward = 7, kCycFinish = 8, kCycSbTiles = 9 };
 
 template <class Op, class T>
 struct ScanImpl {
@@ -75,7 +76,7 @@ struct ScanImpl {
         size_t counters, flags1, flags2, memset_bytes, p1agg, p1inc, p2agg, p2inc, partial;
         int64_t ntiles_c;
         size_t tileF, tileP, chunkRec, counter_c, roundRec, arrive, lbFlags, lbAgg, lbInc, lbTileF, lbTileP, lbPark,
-            total;
+            cycXflag, cycXval, total;
     };
     static Layout layout(int64_t n) {
         Layout L{};
@@ -107,6 +108,9 @@ struct ScanImpl {
         L.lbTileF = off; off += align256((size_t)ntl * W * 8);
         L.lbTileP = off; off += align256((size_t)ntl * W * 8);
         L.lbPark = off; off += align256((size_t)NTL_MIN * (W + MD) * 8);  // the last tile's parked rows
+        // block-cyclic sweep (f1): per round, the incoming carry published by CTA 0
+        L.cycXflag = off; off += align256((size_t)(L.ntiles_c + 1) * 4);
+        L.cycXval = off; off += align256((size_t)(L.ntiles_c + 1) * W * 8);
         L.total = off;
         return L;
     }
@@ -439,6 +443,127 @@ struct ScanImpl {
         return st;
     }
 
+    // ---------------- block-cyclic multi-GPU sweep (scan_sweep.cuh) ----------------
+    // geometry shared by every rank: tiles per superblock (the SB size is the
+    // caller's, identical on all ranks), this rank's local SBs, CTAs
+    static int64_t cyc_tps(const vjp_cyclic &cy) { return cy.sb_elems / TILE_C; }
+    static int64_t cyc_nsb(const vjp_cyclic &cy) { return (cy.global_n + cy.sb_elems - 1) / cy.sb_elems; }
+    static int64_t cyc_nloc(const vjp_cyclic &cy, int rank) {
+        const int64_t nsb = cyc_nsb(cy);
+        return nsb > rank ? (nsb - 1 - rank) / cy.world + 1 : 0;
+    }
+    template <bool FWD, bool ACC, bool YS>
+    static int cyc_occupancy() {
+        constexpr int S = sw_stages<FWD, ACC, YS>();
+        auto k = vjpk::scan_sweep<Op, T, NTC, S, FWD, ACC, YS, true>;
+        const size_t sm = smem_sw<FWD, ACC, YS>();
+        set_smem(k, sm);
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NTC + 64, sm) != cudaSuccess || occ < 1) occ = 1;
+        return occ;
+    }
+    // forward pass (FWD operators): K_F tile aggregates, then per local SB its aggregate -> c.partial [nloc][W]
+    static vjp_status cyc_forward(const ScanCall &c) {
+        if (!need_fwd(c)) return VJP_OK;
+        const vjp_cyclic &cy = *c.cyc;
+        Layout L = layout(c.n);
+        vjpk::ChunkParams p = cparams(c, L, nchunks_fwd(L));
+        CUtensorMap ma, my, mab, mys;
+        if (!maps_c(c, p.full_rows, &ma, &my, &mab, &mys)) return VJP_ECUDA;
+        auto k = vjpk::scan_reduce<Op, T, NTC, SC, true, false>;
+        const size_t sm = smem_r(1);
+        set_smem(k, sm);
+        k<<<(unsigned)p.nchunks, NTC, sm, c.stream>>>(ma, my, p);
+        const int64_t nloc = cyc_nloc(cy, cy.rank);
+        vjpk::scan_cyc_sbagg<Op, NTC><<<(unsigned)nloc, NTC, 0, c.stream>>>(p, (int32_t)cyc_tps(cy),
+                                                                           static_cast<double *>(c.partial));
+        count_launch(2);
+        return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+    }
+    template <bool FWD, bool ACC, bool YS>
+    static vjp_status cyc_launch(const ScanCall &c, const Layout &L) {
+        constexpr int S = sw_stages<FWD, ACC, YS>();
+        constexpr int NTH = NTC + 64;
+        const vjp_cyclic &cy = *c.cyc;
+        auto k = vjpk::scan_sweep<Op, T, NTC, S, FWD, ACC, YS, true>;
+        const size_t sm = smem_sw<FWD, ACC, YS>();
+        set_smem(k, sm);
+        int64_t G = cy.grid_ctas > 0 ? cy.grid_ctas : (int64_t)sm_count() * cyc_occupancy<FWD, ACC, YS>();
+        if (G > kMaxChunks) G = kMaxChunks;
+        const int64_t tps = cyc_tps(cy);
+        if (G > tps) G = tps;  // a CTA per tile at most (keeps R * G records within the workspace)
+        int64_t K = (tps + G - 1) / G;
+        if (K > vjpk::kSweepKMax) return VJP_EINVAL;  // superblock too large for this grid
+        vjpk::SweepParams sp{};
+        sp.c = cparams(c, L, 1);
+        sp.c.global_first = cy.rank == 0 ? 1 : 0;
+        sp.G = (int32_t)G;
+        sp.K = (int32_t)K;
+        sp.R = (int32_t)cyc_nloc(cy, cy.rank);
+        sp.D = 1;
+        unsigned char *ws = static_cast<unsigned char *>(c.ws);
+        sp.roundRec = reinterpret_cast<double *>(ws + L.roundRec);
+        sp.arrive = reinterpret_cast<uint32_t *>(ws + L.arrive);
+        sp.cyc = 1;
+        sp.cw = cy.world;
+        sp.cr = cy.rank;
+        sp.epoch = cy.epoch;
+        sp.tps = (int32_t)tps;
+        sp.nsb = (int32_t)cyc_nsb(cy);
+        for (int q = 0; q < cy.world; ++q) {
+            unsigned char *b = static_cast<unsigned char *>(cy.status[q]);
+            sp.shdr[q] = reinterpret_cast<uint32_t *>(b);
+            sp.sflag[q] = reinterpret_cast<uint32_t *>(b + 256);
+            sp.spay[q] = reinterpret_cast<double *>(b + 256 + align256((size_t)sp.nsb * 4));
+        }
+        sp.err = static_cast<uint32_t *>(cy.status[cy.rank]);  // word 0 of this rank's status buffer
+        sp.xflag = reinterpret_cast<uint32_t *>(ws + L.cycXflag);
+        sp.xval = reinterpret_cast<double *>(ws + L.cycXval);
+        if (cudaMemsetAsync(sp.arrive, 0, (size_t)sp.R * 4, c.stream) != cudaSuccess) return VJP_ECUDA;
+        if (cudaMemsetAsync(sp.xflag, 0, (size_t)sp.R * 4, c.stream) != cudaSuccess) return VJP_ECUDA;
+        CUtensorMap ma, my, mab, mys, mab32, mys32;
+        if (!maps_c(c, sp.c.full_rows, &ma, &my, &mab, &mys)) return VJP_ECUDA;
+        const bool f64 = sizeof(T) == 8;
+        if (!make_row_tmap(&mab32, c.as_bar, sp.c.full_rows, f64, 32)) return VJP_ECUDA;
+        if (!make_row_tmap(&mys32, c.ys, c.ys ? sp.c.full_rows : 0, f64, 32)) return VJP_ECUDA;
+        if (cy.grid_ctas > 0) {
+            // virtual ranks sharing one device: plain launch of a grid the caller
+            // sized so that every rank's CTAs are resident together
+            k<<<(unsigned)G, NTH, sm, c.stream>>>(ma, my, mab, mab32, mys32, sp);
+            count_launch();
+            return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+        }
+        void *args[] = {&ma, &my, &mab, &mab32, &mys32, &sp};
+        cudaError_t e = cudaLaunchCooperativeKernel((const void *)k, dim3((unsigned)G), dim3(NTH), args, sm, c.stream);
+        count_launch();
+        return e == cudaSuccess && cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+    }
+    static vjp_status cyc_finish(const ScanCall &c) {
+        const vjp_cyclic &cy = *c.cyc;
+        Layout L = layout(c.n);
+        const bool fwd = need_fwd(c);
+        const bool acc = (c.flags & VJP_ACCUMULATE) != 0;
+        const bool ys = c.ys != nullptr;
+        if (fwd) {
+            vjpk::ChunkParams p = cparams(c, L, 1);
+            const int64_t nloc = cyc_nloc(cy, cy.rank);
+            const int64_t nloc_max = cyc_nloc(cy, 0);
+            vjpk::scan_cyc_tileprefix<Op, NTC><<<(unsigned)nloc, NTC, 0, c.stream>>>(
+                p, (int32_t)cyc_tps(cy), cy.world, cy.rank, (int32_t)nloc_max, static_cast<const double *>(c.gathered));
+            count_launch();
+            if (cudaGetLastError() != cudaSuccess) return VJP_ECUDA;
+        }
+        if (std::is_same<Op, vjpk::OpAdd>::value && !ys)
+            return acc ? cyc_launch<false, true, false>(c, L) : cyc_launch<false, false, false>(c, L);
+        if (acc) return ys ? cyc_launch<true, true, true>(c, L) : cyc_launch<true, true, false>(c, L);
+        return ys ? cyc_launch<true, false, true>(c, L) : cyc_launch<true, false, false>(c, L);
+    }
+    // tiles per superblock the sweep geometry of this device suggests (K = 4
+    // tiles per CTA, the measured best round for scan(+), DESIGN 7.6)
+    static int64_t cyc_default_sb_tiles() {
+        return (int64_t)sm_count() * cyc_occupancy<!std::is_same<Op, vjpk::OpAdd>::value, false, false>() * 4;
+    }
+
     // ---------------- one-read block look-back (world == 1; scan_blocklb.cuh) ----------------
     static bool use_lb(const ScanCall &c) {
         if (c.world != 1 || (c.flags & VJP_ACCUMULATE)) return false;  // ACCUMULATE: as_bar holds inputs
@@ -750,6 +875,26 @@ vjp_status scan_dispatch(int phase, const ScanCall &c, size_t *out) {
         vjpk::scan_identity_record<Op><<<1, 32, 0, c.stream>>>(static_cast<double *>(c.partial));
         count_launch();
         return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+    }
+    if (phase == kCycSbTiles) {
+        if constexpr (Op::kRevNeedsRs) {
+            *out = 0;
+            return VJP_EUNSUPPORTED;
+        } else {
+            *out = (size_t)(c.dtype == VJP_F64 ? ScanImpl<Op, double>::cyc_default_sb_tiles()
+                                               : ScanImpl<Op, float>::cyc_default_sb_tiles()) *
+                   (size_t)(c.dtype == VJP_F64 ? ScanImpl<Op, double>::TILE_C : ScanImpl<Op, float>::TILE_C);
+            return VJP_OK;
+        }
+    }
+    if (phase == kCycForward || phase == kCycFinish) {
+        if constexpr (Op::kRevNeedsRs) {
+            return VJP_EUNSUPPORTED;  // MIN/MAX: reverse maps depend on the forward carry (two exchanges)
+        } else {
+            if (c.dtype == VJP_F64)
+                return phase == kCycForward ? ScanImpl<Op, double>::cyc_forward(c) : ScanImpl<Op, double>::cyc_finish(c);
+            return phase == kCycForward ? ScanImpl<Op, float>::cyc_forward(c) : ScanImpl<Op, float>::cyc_finish(c);
+        }
     }
     if (c.dtype == VJP_F64) {
         using I = ScanImpl<Op, double>;

@@ -45,6 +45,8 @@ namespace vjpk {
 
 constexpr int kSweepNT = 128;  // tile threads (+ one carry warp)
 
+constexpr int kCycMax = 8;  // ranks of one NVSwitch domain (block-cyclic mode)
+
 struct SweepParams {
     ChunkParams c;      // geometry, arrays, tileP (tileF/chunkRec unused here)
     int32_t G;          // CTAs (all co-resident: cooperative launch)
@@ -53,6 +55,23 @@ struct SweepParams {
     int32_t D;          // reduce look-ahead in rounds (1 or 2)
     double *roundRec;   // [R][G][kMapD] sub-chunk reverse maps
     uint32_t *arrive;   // [R] arrival counters, zeroed before the launch
+    // ---- block-cyclic multi-GPU partition; cyc == 0: one GPU.
+    // The global array is cut into superblocks (SB) of tps tiles; SB J is owned
+    // by rank J % cw and is this rank's local SB J / cw (local arrays are the
+    // owned SBs in order).  Round r = local SB l = R - 1 - r (right to left).
+    // The carry entering SB J comes from SB J + 1 on the NEXT rank: decoupled
+    // look-back over the SB status words every rank pushes to every rank's
+    // status buffer (peer-mapped device memory over NVLink).
+    int32_t cyc, cw, cr;  // mode, world, rank
+    uint32_t epoch;       // status words read (epoch << 2) | state, state 1 = AGG, 2 = INCL
+    int32_t tps;          // tiles per superblock
+    int32_t nsb;          // global superblocks
+    uint32_t *shdr[kCycMax];   // every rank's status header: [0] error word, [1 + q] epoch rank q entered
+    uint32_t *sflag[kCycMax];  // every rank's status words [nsb] (peer pointers)
+    double *spay[kCycMax];     // every rank's payloads [nsb][kMapD + W]: AGG map, INCL carry
+    uint32_t *xflag;           // local [R]: the SB's incoming carry is in xval (CTA 0 -> others)
+    double *xval;              // local [R][W]
+    uint32_t *err;             // local: a look-back wait timed out (results invalid)
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
@@ -93,14 +112,27 @@ __device__ __forceinline__ SweepSeg sweep_seg(int s, int D) {
     const int i = s - D;
     return (i & 1) ? SweepSeg{true, i >> 1} : SweepSeg{false, (i >> 1) + D};
 }
-__device__ __forceinline__ int64_t sweep_q0(const SweepParams &p, int r) {
-    return ((int64_t)r * p.G + blockIdx.x) * p.K;
+// round r spans tiles [sweep_begin, sweep_end); CTA c owns the K tiles
+// counted from the round's right end: tile = end - 1 - (cK + j)
+__device__ __forceinline__ int64_t sweep_end(const SweepParams &p, int r) {
+    if (p.cyc) {
+        const int64_t e = (int64_t)(p.R - r) * p.tps;
+        return e < p.c.ntiles ? e : p.c.ntiles;
+    }
+    return (int64_t)p.c.ntiles - (int64_t)r * p.G * p.K;
+}
+__device__ __forceinline__ int64_t sweep_begin(const SweepParams &p, int r) {
+    if (p.cyc) return (int64_t)(p.R - 1 - r) * p.tps;
+    const int64_t b = (int64_t)p.c.ntiles - (int64_t)(r + 1) * p.G * p.K;
+    return b > 0 ? b : 0;
+}
+__device__ __forceinline__ int64_t sweep_tile(const SweepParams &p, int r, int j) {
+    return sweep_end(p, r) - 1 - ((int64_t)blockIdx.x * p.K + j);
 }
 __device__ __forceinline__ int sweep_nseg(const SweepParams &p) { return p.D + 2 * p.R; }
 __device__ __forceinline__ int sweep_count(const SweepParams &p, int r) {
     if (r >= p.R) return 0;
-    int64_t q0 = sweep_q0(p, r);
-    int64_t left = (int64_t)p.c.ntiles - q0;
+    const int64_t left = sweep_end(p, r) - sweep_begin(p, r) - (int64_t)blockIdx.x * p.K;
     return left <= 0 ? 0 : (left >= p.K ? p.K : (int)left);
 }
 
@@ -154,6 +186,79 @@ __global__ void __launch_bounds__(NT) scan_tile_prefix(const ChunkParams p) {
     }
     V tot;
     V ex = block_excl_fwd<Op, NW>(f, vs, tot);
+    V r = Op::fwd(Fpre, ex);
+    for (int64_t j = t0 + t * per; j < t0 + (t + 1) * per && j < t1; ++j) {
+#pragma unroll
+        for (int q = 0; q < W; ++q) st_cg(p.tileP + j * W + q, r.x[q]);
+        V v;
+#pragma unroll
+        for (int q = 0; q < W; ++q) v.x[q] = ld_cg(p.tileF + j * W + q);
+        r = Op::fwd(r, v);
+    }
+}
+
+// ---- block-cyclic forward re-execution (f1; "the forward sweep is
+// the original scan") --------------------------------------------------------
+// one CTA per local superblock l: its forward aggregate (ordered fold of the
+// K_F tile aggregates tileF over the SB's tiles) -> sbagg[l][W]
+template <class Op, int NT>
+__global__ void __launch_bounds__(NT) scan_cyc_sbagg(const ChunkParams p, int32_t tps, double *__restrict__ sbagg) {
+    using V = typename Op::Val;
+    constexpr int W = Op::W, NW = NT / 32;
+    __shared__ V vs[NW + 1];
+    const int t = threadIdx.x;
+    const int64_t t0 = (int64_t)blockIdx.x * tps;
+    const int64_t t1 = t0 + tps < p.ntiles ? t0 + tps : p.ntiles;
+    const int64_t k = t1 - t0, per = (k + NT - 1) / NT;
+    V f = Op::fwd_id();
+    for (int64_t j = t0 + t * per; j < t0 + (t + 1) * per && j < t1; ++j) {
+        V v;
+#pragma unroll
+        for (int q = 0; q < W; ++q) v.x[q] = ld_cg(p.tileF + j * W + q);
+        f = Op::fwd(f, v);
+    }
+    const V tot = block_reduce_fwd<Op, NW>(f, vs);
+    if (t == 0) {
+#pragma unroll
+        for (int q = 0; q < W; ++q) sbagg[(int64_t)blockIdx.x * W + q] = tot.x[q];
+    }
+}
+// one CTA per local SB l (global J = l * cw + cr): forward prefix entering the
+// SB = ordered fold of every rank's SB aggregates J' < J from the gathered
+// table [cw][nloc_max][W] (SB J' is rank J' % cw's local SB J' / cw), then the
+// exclusive prefixes of the SB's tiles -> tileP
+template <class Op, int NT>
+__global__ void __launch_bounds__(NT) scan_cyc_tileprefix(const ChunkParams p, int32_t tps, int32_t cw, int32_t cr,
+                                                          int32_t nloc_max, const double *__restrict__ gathered) {
+    using V = typename Op::Val;
+    constexpr int W = Op::W, NW = NT / 32;
+    __shared__ V vs[NW + 1];
+    const int t = threadIdx.x;
+    const int64_t J = (int64_t)blockIdx.x * cw + cr;
+    V f = Op::fwd_id();
+    {
+        const int64_t per = (J + NT - 1) / NT;
+        for (int64_t j = t * per; j < (t + 1) * per && j < J; ++j) {
+            const double *g = gathered + ((j % cw) * (int64_t)nloc_max + j / cw) * W;
+            V v;
+#pragma unroll
+            for (int q = 0; q < W; ++q) v.x[q] = g[q];
+            f = Op::fwd(f, v);
+        }
+    }
+    const V Fpre = block_reduce_fwd<Op, NW>(f, vs);
+    const int64_t t0 = (int64_t)blockIdx.x * tps;
+    const int64_t t1 = t0 + tps < p.ntiles ? t0 + tps : p.ntiles;
+    const int64_t k = t1 - t0, per = (k + NT - 1) / NT;
+    f = Op::fwd_id();
+    for (int64_t j = t0 + t * per; j < t0 + (t + 1) * per && j < t1; ++j) {
+        V v;
+#pragma unroll
+        for (int q = 0; q < W; ++q) v.x[q] = ld_cg(p.tileF + j * W + q);
+        f = Op::fwd(f, v);
+    }
+    V tot;
+    const V ex = block_excl_fwd<Op, NW>(f, vs, tot);
     V r = Op::fwd(Fpre, ex);
     for (int64_t j = t0 + t * per; j < t0 + (t + 1) * per && j < t1; ++j) {
 #pragma unroll
@@ -235,7 +340,7 @@ __device__ __forceinline__ void sweep_producer(const SweepParams &sp, uint64_t *
         const int s = (int)(j % S);
         if (j >= S) mbar_wait(&empty[s], (uint32_t)(((j / S) - 1) & 1));
         const SweepSeg sg = sweep_seg(it.s, sp.D);
-        const int64_t tile = (int64_t)sp.c.ntiles - 1 - (sweep_q0(sp, sg.round) + it.j);
+        const int64_t tile = sweep_tile(sp, sg.round, it.j);
         const int rows = chunk_tile_rows<NT>(sp.c, tile);
         const int nb = sg.apply ? NBA : NBR;
         unsigned char *stage = base + s * STG;
@@ -257,6 +362,123 @@ __device__ __forceinline__ void sweep_producer(const SweepParams &sp, uint64_t *
         ++it.j;
         sweep_norm(sp, it);
     }
+}
+
+// ---- block-cyclic look-back (f1) ------------------------------------------
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_sys_u32(uint32_t *p, uint32_t v) {
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys_f64(double *p, double v) {
+    asm volatile("st.relaxed.sys.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ double ld_relaxed_sys_f64(const double *p) {
+    double v;
+    asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+constexpr uint64_t kCycTimeoutNs = 4000000000ull;  // a wait this long means a missing peer: flag and go on
+
+// wait until the status word of SB j (in this rank's buffer) carries this
+// epoch; returns the state (1 AGG, 2 INCL; 0 after a timeout)
+__device__ __forceinline__ uint32_t cyc_wait(const SweepParams &sp, int64_t j) {
+    const uint32_t *f = sp.sflag[sp.cr] + j;
+    uint64_t t0 = 0;
+    for (int it = 0;; ++it) {
+        const uint32_t v = ld_acquire_sys_u32(f);
+        if ((v >> 2) == sp.epoch && (v & 3u)) return v & 3u;
+        if ((it & 63) == 63) {
+            const uint64_t t = globaltimer_ns();
+            if (!t0) t0 = t;
+            else if (t - t0 > kCycTimeoutNs || ld_flag(sp.err)) {  // after one timeout: no more waiting
+                atomicOr(sp.err, 1u);
+                return 0;
+            }
+        }
+        __nanosleep(64);
+    }
+}
+// push (state, payload) of SB J to every rank's status buffer: payload
+// stores (row J of width PR, NP doubles at column off), one sys-scope
+// acq_rel fence, then the status words — a release pattern at sys scope
+template <int PR, int NP>
+__device__ __forceinline__ void cyc_publish(const SweepParams &sp, int64_t J, int off, const double *d,
+                                            uint32_t state) {
+    for (int q = 0; q < sp.cw; ++q)
+#pragma unroll
+        for (int k = 0; k < NP; ++k) st_relaxed_sys_f64(sp.spay[q] + J * PR + off + k, d[k]);
+    fence_acq_rel_sys();
+    for (int q = 0; q < sp.cw; ++q) st_relaxed_sys_u32(sp.sflag[q] + J, (sp.epoch << 2) | state);
+}
+
+// CTA 0's carry warp, lane 0, round r: publish the SB's map M_J (AGG), look
+// back to the right for the carry X_J entering SB J — X_J = M_{J+1} o M_{J+2}
+// o ... applied to the first INCL carry E found (E_j = the carry leaving SB j
+// to the left), or to 0 past the right end (the zero carry of the return
+// sweep's last element) — then publish E_J = M_J(X_J) (INCL)
+template <class Op>
+__device__ typename Op::Val cyc_lookback(const SweepParams &sp, int r, const typename Op::Map &la) {
+    using V = typename Op::Val;
+    using M = typename Op::Map;
+    constexpr int W = Op::W, MD = Op::kMapD, PR = MD + W;
+    const int64_t J = (int64_t)(sp.R - 1 - r) * sp.cw + sp.cr;
+    if (r == 0) {
+        // entry barrier: this call writes status words into every rank's
+        // buffer, so first every rank that owns a superblock must have entered
+        // this epoch — i.e. finished the previous call (stream order) and with
+        // it every read of the previous call's words.  Epochs increase.
+        for (int q = 0; q < sp.cw; ++q) st_relaxed_sys_u32(sp.shdr[q] + 1 + sp.cr, sp.epoch);
+        for (int q = 0; q < sp.cw && q < sp.nsb; ++q) {
+            uint64_t t0 = 0;
+            for (int it = 0; ld_acquire_sys_u32(sp.shdr[sp.cr] + 1 + q) < sp.epoch; ++it) {
+                __nanosleep(64);
+                if ((it & 63) == 63) {
+                    const uint64_t t = globaltimer_ns();
+                    if (!t0) t0 = t;
+                    else if (t - t0 > kCycTimeoutNs || ld_flag(sp.err)) { atomicOr(sp.err, 1u); break; }
+                }
+            }
+        }
+    }
+    double d[MD];
+    map_to<Op>(la, d);
+    cyc_publish<PR, MD>(sp, J, 0, d, 1u);
+    M acc = Op::map_id();
+    V X;
+#pragma unroll
+    for (int q = 0; q < W; ++q) X.x[q] = 0.0;
+    const double *pay = sp.spay[sp.cr];
+    for (int64_t j = J + 1; j < sp.nsb; ++j) {
+        const uint32_t st = cyc_wait(sp, j);
+        if (st == 2u) {
+            V e;
+#pragma unroll
+            for (int q = 0; q < W; ++q) e.x[q] = ld_relaxed_sys_f64(pay + j * PR + MD + q);
+            X = e;
+            break;
+        }
+        double md[MD];
+#pragma unroll
+        for (int q = 0; q < MD; ++q) md[q] = ld_relaxed_sys_f64(pay + j * PR + q);
+        acc = Op::compose(acc, map_from<Op>(md));  // acc o M_j
+    }
+    X = Op::apply(acc, X);
+    const V E = Op::apply(la, X);
+    double e[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) e[q] = E.x[q];
+    cyc_publish<PR, W>(sp, J, MD, e, 2u);
+    return X;
 }
 
 // carry warp (lane-parallel record loads, 8 in flight per lane)
@@ -320,6 +542,35 @@ __device__ __forceinline__ void sweep_carry_warp(const SweepParams &sp, SweepSme
                 la = Op::compose(ua, la);
                 lp = Op::compose(up, lp);
             }
+        }
+        if (sp.cyc) {
+            // block-cyclic: the carry entering this SB comes from the other ranks
+            if (lane == 0) {
+                V X;
+                if (c == 0) {
+                    X = cyc_lookback<Op>(sp, r, la);
+#pragma unroll
+                    for (int q = 0; q < W; ++q) st_cg(sp.xval + (int64_t)r * W + q, X.x[q]);
+                    __threadfence();
+                    red_release_add(sp.xflag + r, 1u);
+                } else {
+                    uint64_t t0 = 0;
+                    for (int it = 0; ld_flag(sp.xflag + r) == 0u; ++it) {
+                        __nanosleep(128);
+                        if ((it & 63) == 63) {
+                            const uint64_t t = globaltimer_ns();
+                            if (!t0) t0 = t;
+                            else if (t - t0 > kCycTimeoutNs || ld_flag(sp.err)) { atomicOr(sp.err, 1u); break; }
+                        }
+                    }
+                    (void)ld_acquire_u32(sp.xflag + r);
+#pragma unroll
+                    for (int q = 0; q < W; ++q) X.x[q] = ld_cg(sp.xval + (int64_t)r * W + q);
+                }
+                sm.carry[slot] = Op::apply(lp, X);
+                mbar_arrive(&sm.carrybar[slot]);
+            }
+            continue;
         }
         if (lane == 0) {
             sm.carry[slot] = Op::apply(lp, Xin);
@@ -388,14 +639,13 @@ __global__ void __launch_bounds__(NT + 64, (FWD || ACC) ? 2 : 3) scan_sweep(cons
         const SweepSeg sg = sweep_seg(s, sp.D);
         if (!sg.apply && sg.round >= sp.R) continue;
         const int cnt = sweep_count(sp, sg.round);
-        const int64_t q0 = sweep_q0(sp, sg.round);
         const int slot = sg.round % kSweepSlots;
         const uint32_t par = (uint32_t)((sg.round / kSweepSlots) & 1);
         const int rslot = sg.round & 1;
         if (!sg.apply) {
             // ------------------------------------------------ R(r): no block barrier per tile
             for (int i = 0; i < cnt; ++i, ++job) {
-                const int64_t tile = (int64_t)p.ntiles - 1 - (q0 + i);
+                const int64_t tile = sweep_tile(sp, sg.round, i);
                 const int st = (int)(job % S);
                 mbar_wait(&ss.full[st], (uint32_t)((job / S) & 1));
                 unsigned char *sA = base + st * STG;
@@ -457,7 +707,7 @@ __global__ void __launch_bounds__(NT + 64, (FWD || ACC) ? 2 : 3) scan_sweep(cons
         mbar_wait(&ss.carrybar[slot], par);
         X = ss.carry[slot];
         for (int i = 0; i < cnt; ++i, ++job) {
-            const int64_t tile = (int64_t)p.ntiles - 1 - (q0 + i);
+            const int64_t tile = sweep_tile(sp, sg.round, i);
             const int st = (int)(job % S);
             const int jp = (int)(job & 1);
             V Ftile = Op::fwd_id();

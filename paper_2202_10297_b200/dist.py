@@ -32,7 +32,8 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-from . import (ACCUMULATE, MAX, MIN, WIDTH, VjpShard, _check, _dt, _it, _op, _p, _stream, lib, workspace)
+from . import (ACCUMULATE, ADD, MAX, MIN, WIDTH, VjpCyclic, VjpShard, _check, _dt, _it, _op, _p, _stream, lib,
+               workspace)
 
 
 def _all_gather_into(out: torch.Tensor, inp: torch.Tensor, group=None):
@@ -53,6 +54,15 @@ def _all_reduce(t: torch.Tensor, op, group=None):
     h = t.cpu()
     dist.all_reduce(h, op=op, group=group)
     t.copy_(h.to(t.device))
+
+
+def cyclic_layout(global_n: int, sb_elems: int, world: int, rank: int) -> list[tuple[int, int]]:
+    """block-cyclic partition (vjp_scan_cyclic): superblock J
+    = global elements [J sb, min((J + 1) sb, global_n)) belongs to rank J %
+    world; a rank's local array is its superblocks in increasing J.  Returns
+    [(global_start, length), ...] in local order."""
+    nsb = -(-global_n // sb_elems) if global_n > 0 else 0
+    return [(J * sb_elems, min((J + 1) * sb_elems, global_n) - J * sb_elems) for J in range(rank, nsb, world)]
 
 
 def shard_bounds(global_n: int, world: int, rank: int) -> tuple[int, int]:
@@ -110,6 +120,96 @@ def scan(op, ys_bar: torch.Tensor, as_: torch.Tensor | None, *, offset: int, glo
     if events:
         events["finish_end"].record()
     return (ab, ys) if want_ys else ab
+
+
+_CYC: dict = {}
+
+
+def _cyclic_status(o: int, global_n: int, sb_elems: int, group, dev):
+    """this rank's status buffer and every rank's (peer-mapped) pointer to its
+    buffer, allocated once per (group, op, sizes) and kept with an epoch
+    counter: torch symmetric memory (NVLink peer mappings) for world > 1."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    key = (id(group), o, global_n, sb_elems, str(dev))
+    st = _CYC.get(key)
+    if st is None:
+        nbytes = lib().vjp_scan_cyclic_status_bytes(o, global_n, sb_elems)
+        if world == 1:
+            buf = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+            st = {"buf": buf, "ptrs": [buf.data_ptr()], "epoch": 0}
+        else:
+            if dist.get_backend(group) != "nccl":
+                raise RuntimeError("scan_cyclic: the status buffers are peer-mapped device memory (NCCL group, "
+                                   "torch symmetric memory); gloo groups use dist.scan")
+            import torch.distributed._symmetric_memory as symm
+            buf = symm.empty(nbytes, dtype=torch.uint8, device=dev)
+            buf.zero_()
+            h = symm.rendezvous(buf, group)
+            torch.cuda.synchronize(dev)
+            h.barrier()
+            st = {"buf": buf, "ptrs": list(h.buffer_ptrs), "epoch": 0, "handle": h}
+        _CYC[key] = st
+    return st
+
+
+def scan_cyclic(op, ys_bar: torch.Tensor, as_: torch.Tensor | None, *, global_n: int, sb_elems: int | None = None,
+                group=None, out: torch.Tensor | None = None, accumulate: bool = False, events: dict | None = None):
+    """vjp_scan over this rank's BLOCK-CYCLIC share of a global scan (SURVEY 8f
+    row f1; include/vjp.h vjp_scan_cyclic): ys_bar / as_ hold the superblocks
+    cyclic_layout(global_n, sb_elems, world, rank) lists, concatenated.  The
+    reverse carries cross ranks inside the kernel (NVLink status words, no
+    collective); MUL / LINREC / MAT2 all-gather the per-superblock forward
+    aggregates first (the forward re-execution's prefix, 8-32 B per superblock)."""
+    o = _op(op)
+    dev = ys_bar.device
+    w = WIDTH[o]
+    n = ys_bar.numel() // w
+    dt = _dt(ys_bar)
+    L = lib()
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if sb_elems is None:
+        sb_elems = L.vjp_scan_cyclic_sb_elems(o, dt)
+    st = _cyclic_status(o, global_n, sb_elems, group, dev)
+    st["epoch"] += 1
+    cy = VjpCyclic()
+    cy.rank, cy.world, cy.global_n, cy.sb_elems, cy.epoch, cy.grid_ctas = rank, world, global_n, sb_elems, st["epoch"], 0
+    for q, ptr in enumerate(st["ptrs"]):
+        cy.status[q] = ptr
+    if n != L.vjp_scan_cyclic_local_n(cy):
+        raise ValueError(f"scan_cyclic: rank {rank} holds {n} elements, the layout gives "
+                         f"{L.vjp_scan_cyclic_local_n(cy)} (dist.cyclic_layout)")
+    ws = workspace(L.vjp_scan_workspace_bytes(o, dt, n), dev)
+    nbytes = 0 if ws is None else ws.numel()
+    s = _stream(dev)
+    gathered = None
+    if o != ADD:
+        fb = L.vjp_scan_cyclic_fwd_bytes(o, dt, cy) // 8
+        sbagg = torch.zeros(fb, dtype=torch.float64, device=dev)
+        _check(L.vjp_scan_cyclic_forward(o, dt, n, _p(as_), _p(ws), nbytes, cy, _p(sbagg), s),
+               "vjp_scan_cyclic_forward")
+        gathered = torch.empty(world * fb, dtype=torch.float64, device=dev)
+        if world > 1:
+            _all_gather_into(gathered, sbagg, group)
+        else:
+            gathered.copy_(sbagg)
+    ab = out if out is not None else torch.empty_like(ys_bar)
+    if events:
+        events["finish_start"].record()
+    _check(L.vjp_scan_cyclic(o, dt, n, _p(as_), _p(ys_bar), _p(ab), _p(ws), nbytes, cy, _p(gathered), s,
+                             ACCUMULATE if accumulate else 0), "vjp_scan_cyclic")
+    if events:
+        events["finish_end"].record()
+    return ab
+
+
+def scan_cyclic_error(global_n: int, op, sb_elems: int, group=None, dev=None) -> int:
+    """word 0 of this rank's status buffer: non-zero if a look-back wait of a
+    previous scan_cyclic call timed out (synchronises)."""
+    st = _CYC.get((id(group), _op(op), global_n, sb_elems, str(dev)))
+    if st is None:
+        return 0
+    return int(st["buf"][:4].view(torch.int32).item())
 
 
 def reduce(op, as_: torch.Tensor, y_bar, *, offset: int, global_n: int, group=None, out=None, want_y=False,

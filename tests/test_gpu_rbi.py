@@ -60,8 +60,12 @@ def test_rbi_golden_g5_g6():
     inds = torch.tensor([0, 1, 0, 1, 2, 2], dtype=torch.int32)
     a = torch.tensor([2, 0, 3, 5, 0, 0], dtype=torch.float64)
     got = vjp.reduce_by_index("mul", inds.to(DEV), a.to(DEV), torch.tensor([1.0, 10, 100], dtype=torch.float64, device=DEV))
-    # the per-bin product is accumulated in the log domain: exact up to rounding (north_star tolerance)
+    # the special-case path forms p_b from fixed-point log2 codes (reading R13b): exact up to
+    # rounding (north_star tolerance); the general rule multiplies exactly: bit-exact
     assert_close(got.cpu().numpy(), np.array([3.0, 50, 2, 0, 0, 0]), np.float64, what="G5")
+    g = vjp.reduce_by_index("mul", inds.to(DEV), a.to(DEV), torch.tensor([1.0, 10, 100], dtype=torch.float64,
+                                                                         device=DEV), general=True)
+    assert g.cpu().tolist() == [3, 50, 2, 0, 0, 0]
     inds = torch.tensor([0, 1, 0, 1, 0], dtype=torch.int32)
     a = torch.tensor([3, 5, 3, -1, 2], dtype=torch.float64)
     got = vjp.reduce_by_index("max", inds.to(DEV), a.to(DEV), torch.tensor([7.0, 9], dtype=torch.float64, device=DEV))
@@ -101,27 +105,36 @@ def test_config4_full_size(op, m):
         assert np.array_equal(got, ref_ab)
 
 
-def test_rbi_mul_log2_accuracy():
-    """the MUL histograms' log2|x| (atanh series) against the correctly rounded
-    value (mpmath-free: long double via numpy on the host is not exact, so use
-    Python's math.log2 on doubles plus a bound): max error <= 2 ulp of the
-    result over wide-range, near-1 and subnormal inputs."""
-    import math
+def test_rbi_mul_code_accuracy():
+    """the MUL histograms' factor codes round(log2|x| 2^51) + [x<0] 2^63
+    (reading R13b) against the exact codes from Python's decimal module (50
+    digits, no floating-point library routine): within 2 quanta (2^-50 on
+    log2) over wide-range, near-1, table-boundary and subnormal inputs; the
+    sign bit exact."""
+    from decimal import Decimal, getcontext
+    getcontext().prec = 50
+    ln2 = Decimal(2).ln()
     x = torch.cat([
-        torch.exp2((synth.uniform(200_000, 90, dtype=torch.float64) - 0.5) * 2000),
-        1.0 + (synth.uniform(200_000, 91, dtype=torch.float64) - 0.5) * 2.0 ** -10,
+        torch.exp2((synth.uniform(20_000, 90, dtype=torch.float64) - 0.5) * 2000),
+        1.0 + (synth.uniform(20_000, 91, dtype=torch.float64) - 0.5) * 2.0 ** -10,
+        1.0 + torch.arange(129, dtype=torch.float64) / 128.0,  # table cell edges
         torch.tensor([1.0, 2.0, 0.5, 3.0, 1e-310, 5e-324, 1.7976931348623157e308, 1.4142135623730951,
-                      1.4142135623730954, 0.7071067811865475], dtype=torch.float64),
+                      1.9999999999999998, 1.0000000000000002, 0.7071067811865475], dtype=torch.float64),
     ])
     x = torch.where(synth.uniform(x.numel(), 92) < 0.5, -x, x)
     xd = x.to("cuda")
-    y = torch.empty_like(xd)
-    vjp._check(vjp.lib().vjp_debug_log2_abs(vjp._p(xd), vjp._p(y), xd.numel(), vjp._stream(xd.device)), "log2")
-    got = y.cpu().numpy()
-    ref = np.array([math.log2(abs(v)) for v in x.numpy()])
-    ulp = np.spacing(np.abs(ref)) + np.where(ref == 0, 5e-324, 0)
-    err = np.abs(got - ref) / ulp
-    assert float(err.max()) <= 2.0, float(err.max())
+    y = torch.empty(xd.numel(), dtype=torch.int64, device="cuda")
+    vjp._check(vjp.lib().vjp_debug_mul_code(vjp._p(xd), vjp._p(y), xd.numel(), vjp._stream(xd.device)), "code")
+    got = [int(v) & ((1 << 64) - 1) for v in y.cpu().tolist()]
+    worst = 0
+    for v, g in zip(x.tolist(), got):
+        exact = (Decimal(abs(v)).ln() / ln2) * (1 << 51)
+        q = int(exact.to_integral_value())
+        expect = (q + ((1 << 63) if v < 0 else 0)) & ((1 << 64) - 1)
+        d = (g - expect) & ((1 << 64) - 1)
+        d = d - (1 << 64) if d >= (1 << 63) else d
+        worst = max(worst, abs(d))
+    assert worst <= 2, worst
 
 
 @pytest.mark.parametrize("it", [torch.int32, torch.int64], ids=["i32", "i64"])
