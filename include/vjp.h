@@ -199,10 +199,13 @@ vjp_status vjp_scan_finish(vjp_op op, vjp_dtype dtype, int64_t n, const void *as
  * SB per round: all CTAs stream the SB once from HBM (the method bytes — no
  * pre-pass over ys_bar, unlike the contiguous split), compose the SB's
  * reverse map M_J, and CTA 0 pushes it (AGG) into EVERY rank's status buffer
- * over NVLink (peer-mapped stores, sys-scope release), looks back over the
- * status words of SBs J+1, J+2, ... (pushed by the other ranks) until an
- * INCL carry is found, and pushes E_J = M_J(X_J) (INCL); the CTAs then apply
- * the SB from L2 with the carry X_J.  No collective call on the ys_bar path.
+ * over NVLink (peer-mapped stores, sys-scope release).  The carry entering
+ * SB J is X_J = M_{J+1} o ... o M_{J+world-1} (E_{J+world}): the maps of the
+ * other ranks' superblocks between J and this rank's previous superblock,
+ * applied to the carry leaving that superblock, which the rank already holds
+ * — so each rank waits only for the other ranks' AGG words (a look-back
+ * terminated locally; no chain of inclusive carries across GPUs).  The CTAs
+ * then apply the SB from L2 with X_J.  No collective on the ys_bar path.
  * For MUL / LINREC / MAT2 the forward re-execution needs each SB's forward
  * prefix: vjp_scan_cyclic_forward writes this rank's per-SB forward
  * aggregates (reads `as` once), the caller all-gathers them (world x

@@ -269,7 +269,8 @@ size_t vjp_scan_cyclic_status_bytes(vjp_op op, int64_t global_n, int64_t sb_elem
     const int64_t nsb = (global_n + sb_elems - 1) / sb_elems;
     const int w = op == VJP_LINREC ? 2 : (op == VJP_MAT2 ? 4 : 1);
     const int md = op == VJP_MAT2 ? 8 : (op == VJP_LINREC ? 3 : (op == VJP_MUL ? 2 : 1));
-    return 256 + align256((size_t)nsb * 4) + align256((size_t)nsb * (md + w) * 8);
+    (void)w;
+    return 256 + align256((size_t)nsb * 4) + align256((size_t)nsb * md * 8);
 }
 
 size_t vjp_scan_cyclic_fwd_bytes(vjp_op op, vjp_dtype dtype, const vjp_cyclic *cy) {

@@ -76,7 +76,7 @@ struct ScanImpl {
         size_t counters, flags1, flags2, memset_bytes, p1agg, p1inc, p2agg, p2inc, partial;
         int64_t ntiles_c;
         size_t tileF, tileP, chunkRec, counter_c, roundRec, arrive, lbFlags, lbAgg, lbInc, lbTileF, lbTileP, lbPark,
-            cycXflag, cycXval, total;
+            total;
     };
     static Layout layout(int64_t n) {
         Layout L{};
@@ -108,9 +108,6 @@ struct ScanImpl {
         L.lbTileF = off; off += align256((size_t)ntl * W * 8);
         L.lbTileP = off; off += align256((size_t)ntl * W * 8);
         L.lbPark = off; off += align256((size_t)NTL_MIN * (W + MD) * 8);  // the last tile's parked rows
-        // block-cyclic sweep (f1): per round, the incoming carry published by CTA 0
-        L.cycXflag = off; off += align256((size_t)(L.ntiles_c + 1) * 4);
-        L.cycXval = off; off += align256((size_t)(L.ntiles_c + 1) * W * 8);
         L.total = off;
         return L;
     }
@@ -517,10 +514,7 @@ struct ScanImpl {
             sp.spay[q] = reinterpret_cast<double *>(b + 256 + align256((size_t)sp.nsb * 4));
         }
         sp.err = static_cast<uint32_t *>(cy.status[cy.rank]);  // word 0 of this rank's status buffer
-        sp.xflag = reinterpret_cast<uint32_t *>(ws + L.cycXflag);
-        sp.xval = reinterpret_cast<double *>(ws + L.cycXval);
         if (cudaMemsetAsync(sp.arrive, 0, (size_t)sp.R * 4, c.stream) != cudaSuccess) return VJP_ECUDA;
-        if (cudaMemsetAsync(sp.xflag, 0, (size_t)sp.R * 4, c.stream) != cudaSuccess) return VJP_ECUDA;
         CUtensorMap ma, my, mab, mys, mab32, mys32;
         if (!maps_c(c, sp.c.full_rows, &ma, &my, &mab, &mys)) return VJP_ECUDA;
         const bool f64 = sizeof(T) == 8;

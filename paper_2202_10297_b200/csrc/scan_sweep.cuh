@@ -59,18 +59,16 @@ struct SweepParams {
     // The global array is cut into superblocks (SB) of tps tiles; SB J is owned
     // by rank J % cw and is this rank's local SB J / cw (local arrays are the
     // owned SBs in order).  Round r = local SB l = R - 1 - r (right to left).
-    // The carry entering SB J comes from SB J + 1 on the NEXT rank: decoupled
-    // look-back over the SB status words every rank pushes to every rank's
-    // status buffer (peer-mapped device memory over NVLink).
+    // The carry entering SB J comes from SB J + 1 on the NEXT rank: look-back
+    // over the SB status words every rank pushes to every rank's status
+    // buffer (peer-mapped device memory over NVLink), see cyc_carry.
     int32_t cyc, cw, cr;  // mode, world, rank
-    uint32_t epoch;       // status words read (epoch << 2) | state, state 1 = AGG, 2 = INCL
+    uint32_t epoch;       // status words read (epoch << 2) | 1 once the SB's map (AGG) is in
     int32_t tps;          // tiles per superblock
     int32_t nsb;          // global superblocks
     uint32_t *shdr[kCycMax];   // every rank's status header: [0] error word, [1 + q] epoch rank q entered
     uint32_t *sflag[kCycMax];  // every rank's status words [nsb] (peer pointers)
-    double *spay[kCycMax];     // every rank's payloads [nsb][kMapD + W]: AGG map, INCL carry
-    uint32_t *xflag;           // local [R]: the SB's incoming carry is in xval (CTA 0 -> others)
-    double *xval;              // local [R][W]
+    double *spay[kCycMax];     // every rank's payloads [nsb][kMapD]: the superblocks' reverse maps
     uint32_t *err;             // local: a look-back wait timed out (results invalid)
 };
 
@@ -390,7 +388,7 @@ __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_re
 constexpr uint64_t kCycTimeoutNs = 4000000000ull;  // a wait this long means a missing peer: flag and go on
 
 // wait until the status word of SB j (in this rank's buffer) carries this
-// epoch; returns the state (1 AGG, 2 INCL; 0 after a timeout)
+// epoch; returns the state (1 = AGG; 0 after a timeout)
 __device__ __forceinline__ uint32_t cyc_wait(const SweepParams &sp, int64_t j) {
     const uint32_t *f = sp.sflag[sp.cr] + j;
     uint64_t t0 = 0;
@@ -421,16 +419,22 @@ __device__ __forceinline__ void cyc_publish(const SweepParams &sp, int64_t J, in
     for (int q = 0; q < sp.cw; ++q) st_relaxed_sys_u32(sp.sflag[q] + J, (sp.epoch << 2) | state);
 }
 
-// CTA 0's carry warp, lane 0, round r: publish the SB's map M_J (AGG), look
-// back to the right for the carry X_J entering SB J — X_J = M_{J+1} o M_{J+2}
-// o ... applied to the first INCL carry E found (E_j = the carry leaving SB j
-// to the left), or to 0 past the right end (the zero carry of the return
-// sweep's last element) — then publish E_J = M_J(X_J) (INCL)
+// Round r of a rank = its superblock J = (R - 1 - r) cw + cr.  The carry
+// entering SB J from the right is X_J = M_{J+1} o M_{J+2} o ... o M_{J+cw-1}
+// (E_{J+cw}): the maps of the cw - 1 superblocks between J and this rank's
+// previous superblock J + cw (owned by the OTHER ranks), applied to the carry
+// E_{J+cw} leaving that previous superblock — which every CTA of this rank
+// already holds (it applied that SB).  So the look-back only ever waits for
+// other ranks' AGG words (published right after their reduce phase: no
+// chain of inclusive values across ranks), and its terminator is local.  In
+// the first round (this rank's rightmost SB) it runs to the right end, where
+// the carry is 0 (the return sweep's zero carry).
+//
+// CTA 0's carry warp, lane 0, first: the entry barrier (r == 0) and the AGG
+// word of SB J (its map la) pushed to every rank.
 template <class Op>
-__device__ typename Op::Val cyc_lookback(const SweepParams &sp, int r, const typename Op::Map &la) {
-    using V = typename Op::Val;
-    using M = typename Op::Map;
-    constexpr int W = Op::W, MD = Op::kMapD, PR = MD + W;
+__device__ void cyc_publish_agg(const SweepParams &sp, int r, const typename Op::Map &la) {
+    constexpr int MD = Op::kMapD;
     const int64_t J = (int64_t)(sp.R - 1 - r) * sp.cw + sp.cr;
     if (r == 0) {
         // entry barrier: this call writes status words into every rank's
@@ -452,33 +456,32 @@ __device__ typename Op::Val cyc_lookback(const SweepParams &sp, int r, const typ
     }
     double d[MD];
     map_to<Op>(la, d);
-    cyc_publish<PR, MD>(sp, J, 0, d, 1u);
+    cyc_publish<MD, MD>(sp, J, 0, d, 1u);
+}
+// every CTA's carry warp, lane 0: X_J from Xprev = E_{J+cw} (r > 0) or 0
+template <class Op>
+__device__ typename Op::Val cyc_carry(const SweepParams &sp, int r, typename Op::Val Xprev) {
+    using V = typename Op::Val;
+    using M = typename Op::Map;
+    constexpr int W = Op::W, MD = Op::kMapD;
+    const int64_t J = (int64_t)(sp.R - 1 - r) * sp.cw + sp.cr;
+    int64_t jend = J + sp.cw;  // this rank's previous superblock (its exit carry is Xprev)
+    if (r == 0) {
+        jend = sp.nsb;  // rightmost SB of this rank: look back to the array's end
+#pragma unroll
+        for (int q = 0; q < W; ++q) Xprev.x[q] = 0.0;
+    }
+    if (jend > sp.nsb) jend = sp.nsb;
     M acc = Op::map_id();
-    V X;
-#pragma unroll
-    for (int q = 0; q < W; ++q) X.x[q] = 0.0;
     const double *pay = sp.spay[sp.cr];
-    for (int64_t j = J + 1; j < sp.nsb; ++j) {
-        const uint32_t st = cyc_wait(sp, j);
-        if (st == 2u) {
-            V e;
-#pragma unroll
-            for (int q = 0; q < W; ++q) e.x[q] = ld_relaxed_sys_f64(pay + j * PR + MD + q);
-            X = e;
-            break;
-        }
+    for (int64_t j = J + 1; j < jend; ++j) {
+        (void)cyc_wait(sp, j);
         double md[MD];
 #pragma unroll
-        for (int q = 0; q < MD; ++q) md[q] = ld_relaxed_sys_f64(pay + j * PR + q);
+        for (int q = 0; q < MD; ++q) md[q] = ld_relaxed_sys_f64(pay + j * MD + q);
         acc = Op::compose(acc, map_from<Op>(md));  // acc o M_j
     }
-    X = Op::apply(acc, X);
-    const V E = Op::apply(la, X);
-    double e[W];
-#pragma unroll
-    for (int q = 0; q < W; ++q) e[q] = E.x[q];
-    cyc_publish<PR, W>(sp, J, MD, e, 2u);
-    return X;
+    return Op::apply(acc, Xprev);
 }
 
 // carry warp (lane-parallel record loads, 8 in flight per lane)
@@ -544,31 +547,14 @@ __device__ __forceinline__ void sweep_carry_warp(const SweepParams &sp, SweepSme
             }
         }
         if (sp.cyc) {
-            // block-cyclic: the carry entering this SB comes from the other ranks
+            // block-cyclic: the carry entering this SB, Xin = E of this rank's previous SB
             if (lane == 0) {
-                V X;
-                if (c == 0) {
-                    X = cyc_lookback<Op>(sp, r, la);
-#pragma unroll
-                    for (int q = 0; q < W; ++q) st_cg(sp.xval + (int64_t)r * W + q, X.x[q]);
-                    __threadfence();
-                    red_release_add(sp.xflag + r, 1u);
-                } else {
-                    uint64_t t0 = 0;
-                    for (int it = 0; ld_flag(sp.xflag + r) == 0u; ++it) {
-                        __nanosleep(128);
-                        if ((it & 63) == 63) {
-                            const uint64_t t = globaltimer_ns();
-                            if (!t0) t0 = t;
-                            else if (t - t0 > kCycTimeoutNs || ld_flag(sp.err)) { atomicOr(sp.err, 1u); break; }
-                        }
-                    }
-                    (void)ld_acquire_u32(sp.xflag + r);
-#pragma unroll
-                    for (int q = 0; q < W; ++q) X.x[q] = ld_cg(sp.xval + (int64_t)r * W + q);
-                }
+                const M lat = la;
+                if (c == 0) cyc_publish_agg<Op>(sp, r, lat);
+                const V X = cyc_carry<Op>(sp, r, Xin);
                 sm.carry[slot] = Op::apply(lp, X);
                 mbar_arrive(&sm.carrybar[slot]);
+                Xin = Op::apply(lat, X);  // E_J: the next round's terminator
             }
             continue;
         }

@@ -120,36 +120,49 @@ def _worker(rank, world, port, q):
         ref = oracle.vjp_scan("min", yv, a)
         np.testing.assert_allclose(out, ref[off:off + n], rtol=1e-14, atol=0)
 
-        # ---- reduce_by_index MAX winners: the 3-step collective protocol ----
-        M, NN = 50, 2000
-        inds, av, hb = synth.rbi_inputs(NN, M, "max")
-        off, n = shard_bounds(NN, world, rank)
-        _, hs_loc, win_loc, _ = oracle.vjp_reduce_by_index("max", inds.numpy()[off:off + n], av.numpy()[off:off + n],
-                                                          hb.numpy())
-        val = torch.from_numpy(np.where(win_loc >= 0, hs_loc, -np.inf))
-        aux = torch.from_numpy(np.where(win_loc >= 0, win_loc + off, np.iinfo(np.int64).max))
-        gval = val.clone()
-        dist.all_reduce(gval, op=dist.ReduceOp.MAX)
-        aux = torch.where(val == gval, aux, torch.full_like(aux, np.iinfo(np.int64).max))
-        dist.all_reduce(aux, op=dist.ReduceOp.MIN)
-        _, _, win_full, _ = oracle.vjp_reduce_by_index("max", inds.numpy(), av.numpy(), hb.numpy())
-        got = aux.numpy().copy()
-        got[got == np.iinfo(np.int64).max] = -1
-        assert np.array_equal(got, win_full)
-        # scatter with ys_bar partitioned (dist.scatter / vjp_scatter_shard): each
-        # rank gathers only the targets it owns (shifted to local indices, the
-        # others out of range -> 0), SUM all_reduce of vs_bar; xs_bar per slice
-        NS, MS = 50_021, 9_000
-        is_, ybs = synth.scatter_inputs(NS, MS, oob=3)
-        off, n = shard_bounds(NS, world, rank)
-        loc = is_.numpy() - off
-        loc = np.where((loc >= 0) & (loc < n), loc, n + 1)  # not owned: out of range (reading R4)
-        xb_loc, vb_loc, _ = oracle.vjp_scatter(loc, ybs.numpy()[off:off + n].copy())
-        vb = torch.from_numpy(vb_loc.copy())
-        dist.all_reduce(vb, op=dist.ReduceOp.SUM)
-        rx, rv, _ = oracle.vjp_scatter(is_.numpy(), ybs.numpy())
-        assert np.array_equal(vb.numpy(), rv)
-        assert np.array_equal(xb_loc, rx[off:off + n])
+        # ---- reduce_by_index and scatter THROUGH dist.* (the module's own
+        # sequencing, buffers and gloo collectives), with the kernels replaced by
+        # CPU fakes of their documented contracts (tests/_fake_lib.py) ----------
+        import paper_2202_10297_b200.dist as vdist
+        from _fake_lib import FakeLib
+        real_lib, real_stream = vdist.lib, vdist._stream
+        vdist.lib = lambda: FakeLib()
+        vdist._stream = lambda dev: None
+        try:
+            for op, M, NN in (("max", 50, 2000), ("min", 37, 1500), ("mul", 40, 1200), ("add", 30, 900)):
+                inds, av, hb = synth.rbi_inputs(NN, M, op)
+                if op == "mul":  # signed factors: the exchange must carry the sign parity
+                    av = torch.where(synth.uniform(NN, 55) < 0.3, -av, av)
+                off, n = shard_bounds(NN, world, rank)
+                got = vdist.reduce_by_index(op, inds[off:off + n].clone(), av[off:off + n].clone(), hb.clone(),
+                                            offset=off, global_n=NN)
+                ref = oracle.vjp_reduce_by_index(op, inds.numpy(), av.numpy(), hb.numpy())[0][off:off + n]
+                if op == "mul":
+                    np.testing.assert_allclose(got.numpy(), ref, rtol=1e-10, atol=0)
+                else:
+                    assert np.array_equal(got.numpy(), ref), op
+            NS, MS = 5_021, 900
+            is_, ybs = synth.scatter_inputs(NS, MS, oob=3)
+            off, n = shard_bounds(NS, world, rank)
+            xb, vb = vdist.scatter(is_, ybs[off:off + n].clone(), offset=off, global_n=NS)
+            rx, rv, _ = oracle.vjp_scatter(is_.numpy(), ybs.numpy())
+            assert np.array_equal(vb.numpy(), rv)
+            assert np.array_equal(xb.numpy(), rx[off:off + n])
+        finally:
+            vdist.lib, vdist._stream = real_lib, real_stream
+        # ---- block-cyclic layout (f1): the ranks' superblocks tile [0, N) once,
+        # and the library's local-size query agrees with the Python layout ------
+        for NN, sb in ((100_000, 4096), (4096 * 7, 4096), (5, 4096), (0, 4096)):
+            spans = vdist.cyclic_layout(NN, sb, world, rank)
+            cy = vjp.VjpCyclic()
+            cy.rank, cy.world, cy.global_n, cy.sb_elems = rank, world, NN, sb
+            assert L.vjp_scan_cyclic_local_n(cy) == sum(ln for _, ln in spans)
+            mine = torch.zeros(NN, dtype=torch.int64)
+            for g0, ln in spans:
+                assert (g0 // sb) % world == rank
+                mine[g0:g0 + ln] += 1
+            dist.all_reduce(mine)
+            assert bool((mine == 1).all())
         dist.barrier()
         dist.destroy_process_group()
         q.put((rank, "ok"))
