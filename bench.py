@@ -143,18 +143,53 @@ def dist_env():
     return world, rank, local
 
 
+def host_info():
+    """the box's host CPU (lscpu model name) and core count, for cpu_baseline"""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.lower().startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    if model is None:
+        try:
+            for ln in open("/proc/cpuinfo"):
+                if ln.lower().startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+        except Exception:
+            pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
 def cpu_oracle_sample(n: int, reps: int = 1):
-    """oracle (plain CPU definition, one thread) on LINREC+MAT2 samples of n elements."""
+    """oracle (plain CPU definition, one thread) on LINREC+MAT2 samples of n
+    elements, the calling thread pinned to one core (sched_setaffinity, the
+    in-process equivalent of taskset -c) and timed with a monotonic clock
+    (time.perf_counter, like std::chrono::steady_clock)."""
     import oracle
     import synth
     a1, y1 = synth.linrec_inputs(n)
     a2, y2 = synth.mat2_inputs(n)
     a1, y1, a2, y2 = a1.numpy(), y1.numpy(), a2.numpy(), y2.numpy()
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        oracle.vjp_scan("linrec", y1, a1)
-        oracle.vjp_scan("mat2", y2, a2)
-    dt = (time.perf_counter() - t0) / reps
+    old = None
+    try:
+        old = os.sched_getaffinity(0)
+        os.sched_setaffinity(0, {min(old)})
+    except Exception:
+        old = None
+    try:
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            oracle.vjp_scan("linrec", y1, a1)
+            oracle.vjp_scan("mat2", y2, a2)
+        dt = (time.perf_counter() - t0) / reps
+    finally:
+        if old is not None:
+            os.sched_setaffinity(0, old)
     return 2 * n / dt, dt
 
 
@@ -180,7 +215,8 @@ def run_reference(args):
                    "sample": f"bounded: each step runs n = 2^22 elements per op ({n} of the 2^26), "
                              "the metric is per element so it is comparable"},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"LINREC+MAT2 n=2^22 each per step, {args.steps} steps"},
+                         "sample": f"LINREC+MAT2 n=2^22 each per step, {args.steps} steps, one thread pinned to "
+                                   "one core", **host_info()},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -234,16 +270,61 @@ def measure_targets(args, dev, peak):
     one("LINREC f64 2^30", "vjp_scan LINREC, n = 2^30 f64", N30, 64 * N30,
         lambda: vjp.scan("linrec", yb, a, out=ab))
     del a, yb, ab
+    l2 = None
     for m in (1000, 1_000_000):
         for op, nb in (("add", 12), ("mul", 32), ("max", 20)):
             inds, a, hb = synth.rbi_inputs(N28, m, op, device=dev)
             o = torch.empty(N28, dtype=torch.float64, device=dev)
+            if m == 1_000_000 and l2 is None:
+                l2 = l2_ceilings(inds, m, dev)
             one(f"rbi {op} m={m}", f"vjp_reduce_by_index {op.upper()}, n = 2^28 f64, int32 bins, m = {m} "
                 "(config 4, uniform bins)", N28, nb * N28,
                 lambda op=op, inds=inds, a=a, hb=hb, o=o: vjp.reduce_by_index(op, inds, a, hb, out=o))
+            if m == 1_000_000:
+                # L2-bound kernels: the calibrated time of their random-access
+                # passes (+: one gather pass; x: one reduction pass + one
+                # gather pass; max: one gather pass, the filter read — its
+                # reductions are rare) over the measured time
+                passes = {"add": l2["gather_ms"], "mul": l2["red_ms"] + l2["gather_ms"], "max": l2["gather_ms"]}[op]
+                out[-1]["l2_bound_ms"] = passes
+                out[-1]["frac_l2"] = passes / out[-1]["ms"]
             del inds, a, hb, o
+    out.append({"name": "L2 ceilings (calibration)", **l2})
     torch.cuda.empty_cache()
     return out
+
+
+def l2_ceilings(inds, m, dev):
+    """calibration (vjp_calib_*): 2^28 random 8-byte gathers / f64 red.adds
+    into an m-entry (8 MB at m = 10^6) L2-resident table, bins streamed as in
+    the histogram kernels; CUDA events, median of 5 after 2 warm-ups."""
+    import torch
+
+    import paper_2202_10297_b200 as vjp
+
+    L = vjp.lib()
+    n = inds.numel() - inds.numel() % 4
+    table = torch.ones(m, dtype=torch.float64, device=dev)
+    olen = L.vjp_calib_out_len()
+    outb = torch.empty(olen, dtype=torch.float64, device=dev)
+    res = {}
+    for name, fn in (("gather_ms", lambda: L.vjp_calib_l2_gather(vjp._p(table), vjp._p(inds), n, vjp._p(outb), olen,
+                                                                 vjp._stream(dev))),
+                     ("red_ms", lambda: L.vjp_calib_l2_red(vjp._p(table), vjp._p(inds), n, vjp._stream(dev)))):
+        for _ in range(2):
+            assert fn() == 0
+        ts = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            assert fn() == 0
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        res[name] = statistics.median(ts)
+    res.update({"n": n, "m": m, "gathers_per_s": n / (res["gather_ms"] * 1e-3),
+                "reds_per_s": n / (res["red_ms"] * 1e-3)})
+    return res
 
 
 def run_ours(args):
@@ -326,13 +407,16 @@ def run_ours(args):
                                                                                   pin_memory=True))
         h2d = sum(h[0].numel() * h[0].element_size() + h[1].numel() * h[1].element_size() for h in host.values())
         d2h = sum(h[2].numel() * h[2].element_size() for h in host.values())
-        e2e_steps = max(1, min(3, args.steps))
+        e2e_steps = max(1, min(4, args.steps))
         for op in ops:  # warm
             vjp.scan(op, host[op][1], host[op][0], out=host[op][2])
+            if world == 1:
+                vjp.scan(op, host[op][1], host[op][0], out=host[op][2], sync=False).wait()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
+        pend = []
         for _ in range(e2e_steps):
             for op in ops:
                 if world > 1:
@@ -342,7 +426,12 @@ def run_ours(args):
                     host[op][2].copy_(ab_d, non_blocking=True)
                     torch.cuda.synchronize()
                 else:
-                    vjp.scan(op, host[op][1], host[op][0], out=host[op][2])
+                    # the public API's asynchronous host-buffer call: copy-in,
+                    # kernels and copy-out on their own streams, so one call's
+                    # copy-out overlaps the next call's copy-in (full-duplex PCIe)
+                    pend.append(vjp.scan(op, host[op][1], host[op][0], out=host[op][2], sync=False))
+        for p_ in pend:
+            p_.wait()
         torch.cuda.synchronize()
         e2e_s = (time.perf_counter() - t0) / e2e_steps
         te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
@@ -350,7 +439,10 @@ def run_ours(args):
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_s = float(te.item())
         e2e = {"value": 2 * gN / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": e2e_s * 1e3, "steps": e2e_steps}
+               "ms_per_step": e2e_s * 1e3, "steps": e2e_steps,
+               "path": "vjp.scan on pinned host buffers" + (", sync=False: copy-in / kernels / copy-out on three "
+                                                           "streams, consecutive calls overlapped" if world == 1
+                                                           else " via dist.scan, synchronous")}
 
     if rank == 0:
         peak, peak_src = peaks()
@@ -368,7 +460,8 @@ def run_ours(args):
         if not args.no_cpu_baseline and world == 1:
             v, dt = cpu_oracle_sample(1 << 23)
             cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                   "sample": "LINREC + MAT2, n = 2^23 each, one pass of the oracle (one host thread)"}
+                   "sample": "LINREC + MAT2, n = 2^23 each, one pass of the oracle (one host thread pinned "
+                             "to one core)", **host_info()}
         line = {
             "metric": METRIC, "value": 2 * gN / (mean_ms * 1e-3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_ms, "higher_is_better": True,

@@ -513,6 +513,19 @@ vjp_status vjp_kmeans(vjp_dtype dtype, int64_t n, int64_t k, int64_t d, const vo
                       int32_t *assign, int64_t *counts, void *cost, void *ws, size_t ws_bytes,
                       vjp_stream_t stream, unsigned flags);
 
+/* ======================================================================
+ * Calibration (measurement only, no vjp): the L2 ceilings the m = 10^6
+ * reduce_by_index kernels are compared against (DESIGN 7.4, bench.py
+ * --workload rbi): n random 8-byte gathers (vjp_calib_l2_gather, out: one
+ * partial sum per thread, vjp_calib_out_len() doubles) or f64 red.adds
+ * (vjp_calib_l2_red) into an L2-resident table, bins int32 read by 128-bit
+ * loads as the histogram kernels do.  n % 4 == 0; idx entries in range.
+ * ==================================================================== */
+int64_t vjp_calib_out_len(void);
+vjp_status vjp_calib_l2_gather(const double *table, const int32_t *idx, int64_t n, double *out, int64_t out_len,
+                               vjp_stream_t stream);
+vjp_status vjp_calib_l2_red(double *table, const int32_t *idx, int64_t n, vjp_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -102,6 +102,9 @@ def lib():
             "vjp_debug_mul_code": ([vp, vp, i64, vp], ci),
             "vjp_scan_batched": ([ci, ci, i64, i64, vp, vp, vp, vp, sz, vp, u32], ci),
             "vjp_kmeans": ([ci, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp, u32], ci),
+            "vjp_calib_out_len": ([], i64),
+            "vjp_calib_l2_gather": ([vp, vp, i64, vp, i64, vp], ci),
+            "vjp_calib_l2_red": ([vp, vp, i64, vp], ci),
             "vjp_scan_cyclic_tile_elems": ([ci, ci], i64),
             "vjp_scan_cyclic_sb_elems": ([ci, ci], i64),
             "vjp_scan_cyclic_local_n": ([cy], i64),
@@ -225,11 +228,70 @@ def _host_out(t: torch.Tensor, like_host: bool):
     return out
 
 
+# ------------------------------------------------- asynchronous host path
+_XSTREAMS: dict = {}
+
+
+def _xstreams(dev):
+    """(copy-in, compute, copy-out) streams of a device for the async host path"""
+    k = str(dev)
+    if k not in _XSTREAMS:
+        _XSTREAMS[k] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+    return _XSTREAMS[k]
+
+
+class Pending:
+    """an in-flight asynchronous host-buffer call; .wait() returns its output"""
+
+    def __init__(self, done: torch.cuda.Event, out: torch.Tensor, keep):
+        self.done, self.out, self._keep = done, out, keep
+
+    def wait(self) -> torch.Tensor:
+        self.done.synchronize()
+        self._keep = None
+        return self.out
+
+
+def _scan_host_async(o: int, ys_bar: torch.Tensor, as_, out, accumulate: bool) -> Pending:
+    if out is None or out.is_cuda or not out.is_pinned() or not ys_bar.is_pinned() or \
+            (as_ is not None and not as_.is_pinned()):
+        raise ValueError("scan(sync=False): pinned host ys_bar / as_ / out are required")
+    if accumulate:
+        raise ValueError("scan(sync=False): accumulate is not supported on the host path")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    _check_out(out, ys_bar.numel(), ys_bar.dtype, dev)
+    w = WIDTH[o]
+    n = ys_bar.numel() // w
+    s_in, s_c, s_out = _xstreams(dev)
+    s_in.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(s_in):
+        yb = ys_bar.to(dev, non_blocking=True)
+        a = None if as_ is None else as_.to(dev, non_blocking=True)
+    s_c.wait_stream(s_in)
+    L = lib()
+    with torch.cuda.stream(s_c):
+        ab = torch.empty_like(yb)
+        ws = workspace(L.vjp_scan_workspace_bytes(o, _dt(yb), n), dev)
+        _check(L.vjp_scan(o, _dt(yb), n, _p(a), _p(yb), _p(ab), None, _p(ws), 0 if ws is None else ws.numel(),
+                          ctypes.c_void_p(s_c.cuda_stream), 0), "vjp_scan")
+    s_out.wait_stream(s_c)
+    with torch.cuda.stream(s_out):
+        out.copy_(ab, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(s_out)
+    # keep the device buffers alive until the copy-out has run (tensors were
+    # allocated on s_in / s_c and are used on later streams)
+    for t in (yb, a, ab, ws):
+        if t is not None:
+            t.record_stream(s_out)
+    return Pending(done, out, (yb, a, ab, ws))
+
+
 # ----------------------------------------------------------------- calls
 
 def scan(op, ys_bar: torch.Tensor, as_: torch.Tensor | None = None, *, out: torch.Tensor | None = None,
          want_ys: bool = False, accumulate: bool = False, lookback: bool = False, sweep: bool = False, chunked: bool = False,
-         blocklb: bool = False):
+         blocklb: bool = False, sync: bool = True):
     """as_bar of ``ys = scan op as_`` with output adjoint ``ys_bar`` (sec 5.2).
 
     Tensors hold n elements of the operator's width (LINREC: (d, c) pairs,
@@ -238,8 +300,18 @@ def scan(op, ys_bar: torch.Tensor, as_: torch.Tensor | None = None, *, out: torc
     the single-sweep decoupled look-back kernels, sweep=True the one-read
     L2-round sweep, chunked=True the two chunked kernels, blocklb=True the
     one-read block look-back (tuning/testing; the default on one GPU is the
-    block look-back, and the L2-round sweep for f64 scan(+) without ys)."""
+    chunked pair, and the L2-round sweep for f64 scan(+) without ys).
+
+    HOST tensors (the end-to-end path): inputs are copied to the device, the
+    result back.  With ``sync=False`` and a pinned host ``out`` the call
+    returns a Pending at once: its host->device copies, kernels and
+    device->host copy run on three per-device streams (copy-in, compute,
+    copy-out) ordered by events, so consecutive calls overlap one call's
+    copy-out with the next one's copy-in (PCIe is full duplex) and the
+    kernels; ``Pending.wait()`` (or torch.cuda.synchronize()) completes it."""
     o = _op(op)
+    if not sync and not ys_bar.is_cuda:
+        return _scan_host_async(o, ys_bar, as_, out, accumulate)
     host = not ys_bar.is_cuda
     dev = _dev_of(ys_bar, as_, out)
     yb = _to(ys_bar, dev)

@@ -258,3 +258,21 @@ def test_scan_minmax_special_values(op):
     for kw in ({}, {"lookback": True}):
         got = vjp.scan(op, yb.to(DEV), a.to(DEV), **kw).cpu().numpy()
         assert_close(got, ref, np.float64, what=f"{op} special {kw}")
+
+
+def test_scan_host_async_pipeline():
+    """the asynchronous host-buffer path (sync=False): several calls in flight
+    on the copy-in / compute / copy-out streams give the synchronous results"""
+    outs, refs = [], []
+    for k, op in enumerate(["linrec", "mat2", "add", "linrec"]):
+        n = 100_003 + 1000 * k
+        a, yb = make(op, n, np.float64)
+        a = None if a is None else a.pin_memory()
+        yb = yb.pin_memory()
+        out = torch.empty(yb.shape, dtype=yb.dtype, pin_memory=True)
+        outs.append((vjp.scan(op, yb, a, out=out, sync=False), out))
+        refs.append(vjp.scan(op, yb.to(DEV), None if a is None else a.to(DEV)).cpu())
+    for (p, out), ref in zip(outs, refs):
+        got = p.wait()
+        assert got.data_ptr() == out.data_ptr()
+        assert torch.equal(got, ref)
