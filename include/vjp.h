@@ -329,15 +329,19 @@ vjp_status vjp_reduce_finish(vjp_op op, vjp_dtype dtype, int64_t n, const void *
  * return VJP_EUNSUPPORTED (see vjp_reduce_by_index_general for MUL).
  *   inds   [n] int32/int64 bins;  as [n x width];  hs_bar [m x width];
  *   as_bar [n x width] output.
- *   hs     nullable DEVICE [m x width]: primal histogram (ADD: sum by
- *          atomic adds — rounding order-dependent; MUL: product; MIN/MAX:
- *          extremum, +-inf for an empty (bin, component)).
+ *   hs     nullable DEVICE [m x width]: primal histogram (ADD: the sum —
+ *          DETERMINISTIC (stable bin sort + in-order segmented row sums,
+ *          the routine vjp_kmeans accumulates its centers with) when ws
+ *          holds vjp_reduce_by_index_hs_workspace_bytes (m <= 12287,
+ *          n < 2^31), else by atomic adds (rounding order-dependent); MUL:
+ *          product; MIN/MAX: extremum, +-inf for an empty (bin, component)).
  *   winners nullable DEVICE int64[m x width]: MIN/MAX winner ELEMENT index
  *          (-1 empty), MUL: zero count, ADD: -1.
  * Errors: VJP_EINVAL (width < 1, m < 1, NULL inputs), VJP_EUNSUPPORTED
  * (LINREC/MAT2), VJP_EALIGN, VJP_EWORKSPACE, VJP_ECUDA.
  * ==================================================================== */
 size_t vjp_reduce_by_index_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_t n, int64_t m, int64_t width);
+size_t vjp_reduce_by_index_hs_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_t n, int64_t m, int64_t width);
 vjp_status vjp_reduce_by_index(vjp_op op, vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, int64_t width,
                                const void *inds, const void *as, const void *hs_bar,
                                void *as_bar, void *hs, int64_t *winners, void *ws,

@@ -86,6 +86,7 @@ def lib():
             "vjp_reduce_partial": ([ci, ci, i64, vp, vp, sz, sp, vp, vp], ci),
             "vjp_reduce_finish": ([ci, ci, i64, vp, vp, vp, vp, vp, vp, sz, sp, vp, vp, u32], ci),
             "vjp_reduce_by_index_workspace_bytes": ([ci, ci, i64, i64, i64], sz),
+            "vjp_reduce_by_index_hs_workspace_bytes": ([ci, ci, i64, i64, i64], sz),
             "vjp_reduce_by_index": ([ci, ci, ci, i64, i64, i64, vp, vp, vp, vp, vp, vp, vp, sz, vp, u32], ci),
             "vjp_reduce_by_index_partial": ([ci, ci, ci, i64, i64, vp, vp, vp, sz, sp, vp, vp, vp], ci),
             "vjp_reduce_by_index_select": ([ci, i64, vp, vp, vp, vp], ci),
@@ -423,7 +424,8 @@ def reduce_by_index(op, inds: torch.Tensor, as_: torch.Tensor | None, hs_bar: to
             torch.cuda.current_stream(dev).synchronize()
             return out
         return _host_out(ab, host)
-    ws = workspace(L.vjp_reduce_by_index_workspace_bytes(o, _dt(hb), n, m, width), dev)
+    wsq = L.vjp_reduce_by_index_hs_workspace_bytes if want_hs else L.vjp_reduce_by_index_workspace_bytes
+    ws = workspace(wsq(o, _dt(hb), n, m, width), dev)
     _check(L.vjp_reduce_by_index(o, _dt(hb), _it(ix), n, m, width, _p(ix), _p(a), _p(hb), _p(ab), _p(hs), _p(win),
                                  _p(ws), 0 if ws is None else ws.numel(), _stream(dev),
                                  ACCUMULATE if accumulate else 0),

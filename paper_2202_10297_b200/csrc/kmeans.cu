@@ -30,6 +30,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "binsort.cuh"
 
 namespace vjpk {
 
@@ -446,193 +447,6 @@ __global__ void __launch_bounds__(KM_MMA_NT, 2) km_assign_mma(const T *__restric
     if (t == 0) cost_part[blockIdx.x] = ((hv[0] + hv[1]) + hv[2]) + hv[3];
 }
 
-__global__ void km_hist(const int32_t *__restrict__ assign, int64_t n, int64_t k, int32_t *__restrict__ hist) {
-    extern __shared__ int32_t h[];
-    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) h[j] = 0;
-    __syncthreads();
-    const int64_t b0 = (int64_t)blockIdx.x * KM_BH;
-    for (int64_t i = b0 + threadIdx.x; i < b0 + KM_BH && i < n; i += blockDim.x) atomicAdd(h + assign[i], 1);
-    __syncthreads();
-    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) hist[(int64_t)blockIdx.x * k + j] = h[j];
-}
-
-// per center (column): exclusive scan over the blocks in place, column total.
-// CTA = 32 centers (x, coalesced) x 32 block segments (y): segment sums, a
-// scan of the 32 segment sums in shared memory, then the in-place rewrite.
-__global__ void __launch_bounds__(1024) km_colscan(int32_t *__restrict__ hist, int64_t nb, int64_t k,
-                                                   int32_t *__restrict__ colsum) {
-    __shared__ int32_t seg[32][33];
-    const int x = threadIdx.x & 31, y = threadIdx.x >> 5;
-    const int64_t j = (int64_t)blockIdx.x * 32 + x;
-    const int64_t per = (nb + 31) / 32, b0 = y * per, b1 = b0 + per < nb ? b0 + per : nb;
-    int32_t s = 0;
-    if (j < k) {
-#pragma unroll 8
-        for (int64_t b = b0; b < b1; ++b) s += hist[b * k + j];
-    }
-    seg[y][x] = s;
-    __syncthreads();
-    if (y == 0) {
-        int32_t run = 0;
-        for (int q = 0; q < 32; ++q) {
-            const int32_t v = seg[q][x];
-            seg[q][x] = run;
-            run += v;
-        }
-        if (j < k) colsum[j] = run;
-    }
-    __syncthreads();
-    if (j < k) {
-        int32_t run = seg[y][x];
-        for (int64_t b = b0; b < b1; ++b) {
-            const int32_t v = hist[b * k + j];
-            hist[b * k + j] = run;
-            run += v;
-        }
-    }
-}
-
-// exclusive scan of the column totals (one CTA of 1024 threads): start[j], start[k] = n
-__global__ void __launch_bounds__(1024) km_startscan(const int32_t *__restrict__ colsum, int64_t k,
-                                                     int32_t *__restrict__ start, int64_t *__restrict__ counts,
-                                                     int acc_counts) {
-    __shared__ int32_t wsum[32];
-    __shared__ int32_t carry;
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    if (t == 0) carry = 0;
-    __syncthreads();
-    for (int64_t base = 0; base < k; base += 1024) {
-        const int64_t j = base + t;
-        const int32_t v = j < k ? colsum[j] : 0;
-        int32_t x = v;
-        for (int o = 1; o < 32; o <<= 1) {
-            const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) wsum[w] = x;
-        __syncthreads();
-        if (w == 0) {
-            int32_t s = wsum[lane];
-            for (int o = 1; o < 32; o <<= 1) {
-                const int32_t y = __shfl_up_sync(0xffffffffu, s, o);
-                if (lane >= o) s += y;
-            }
-            wsum[lane] = s;  // inclusive over warps
-        }
-        __syncthreads();
-        const int32_t excl = carry + (w ? wsum[w - 1] : 0) + x - v;
-        if (j < k) {
-            start[j] = excl;
-            if (counts) counts[j] = (acc_counts ? counts[j] : 0) + v;
-        }
-        __syncthreads();
-        if (t == 1023) carry = excl + v;
-        __syncthreads();
-    }
-    if (t == 0) start[k] = carry;
-}
-
-// stable counting-sort scatter: one warp per block of KM_BH points, in index order
-__global__ void km_order(const int32_t *__restrict__ assign, int64_t n, int64_t k, const int32_t *__restrict__ hist,
-                         const int32_t *__restrict__ start, int32_t *__restrict__ order, int64_t nb) {
-    extern __shared__ int32_t cnt[];  // [warps][k]
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int64_t b = (int64_t)blockIdx.x * nw + w;
-    int32_t *c = cnt + (int64_t)w * k;
-    for (int64_t j = lane; j < k; j += 32) c[j] = 0;
-    __syncwarp();
-    if (b >= nb) return;
-    const int64_t b0 = b * KM_BH;
-    const unsigned lt = (1u << lane) - 1u;
-    const int64_t b1 = b0 + KM_BH < n ? b0 + KM_BH : n;
-    int32_t an = (b0 + lane < b1) ? __ldg(assign + b0 + lane) : -1;
-    for (int64_t i0 = b0; i0 < b1; i0 += 32) {
-        const int64_t i = i0 + lane;
-        const bool in = i < b1;
-        const int32_t a = an;
-        an = (i + 32 < b1) ? __ldg(assign + i + 32) : -1;  // next round in flight
-        const unsigned act = __ballot_sync(0xffffffffu, in);
-        const unsigned peers = __match_any_sync(0xffffffffu, a) & act;
-        int32_t base = 0;
-        if (in) base = c[a];
-        __syncwarp();
-        if (in) {
-            const int32_t r = base + __popc(peers & lt);
-            order[start[a] + hist[b * k + a] + r] = (int32_t)i;
-            if ((peers & lt) == 0) c[a] = base + __popc(peers);  // group leader
-        }
-        __syncwarp();
-    }
-}
-
-// one warp per center: in-order sum of (c_j - p) over the center's segment
-// one CTA of KM_SEGW warps per center: warp w sums its contiguous quarter of
-// the center's (index-ordered) segment, 16 rows in flight; the partials are
-// added in warp order — a fixed order, so the result stays deterministic
-constexpr int KM_SEGW = 4;
-template <class T, int KM_RMAX>
-__global__ void __launch_bounds__(32 * KM_SEGW) km_segsum(const T *__restrict__ P, const T *__restrict__ C,
-                                                         const int32_t *__restrict__ order,
-                                                         const int32_t *__restrict__ start, int64_t k, int64_t d,
-                                                         const T *__restrict__ cost_bar, T *__restrict__ Cbar,
-                                                         T *__restrict__ H, int acc) {
-    __shared__ double part[KM_SEGW][32 * KM_RMAX];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t j = blockIdx.x;
-    const double ybar = (double)*cost_bar;
-    const int32_t s0 = start[j], s1 = start[j + 1];
-    const int32_t len = s1 - s0, per = (len + KM_SEGW - 1) / KM_SEGW;
-    const int32_t w0 = s0 + min(len, w * per), w1 = s0 + min(len, (w + 1) * per);
-    const double two_y = 2.0 * ybar;
-    for (int64_t dc = 0; dc < d; dc += 32 * KM_RMAX) {
-        double cj[KM_RMAX], g[KM_RMAX];
-#pragma unroll
-        for (int r = 0; r < KM_RMAX; ++r) {
-            const int64_t t = dc + lane + 32 * r;
-            cj[r] = t < d ? (double)C[j * d + t] : 0.0;
-            g[r] = 0.0;
-        }
-        for (int32_t s = w0; s < w1; s += KM_SEGB) {
-            int32_t pi[KM_SEGB];
-#pragma unroll
-            for (int u = 0; u < KM_SEGB; ++u) pi[u] = (s + u < w1) ? __ldg(order + s + u) : -1;
-            double v[KM_SEGB][KM_RMAX];
-#pragma unroll
-            for (int u = 0; u < KM_SEGB; ++u)
-#pragma unroll
-                for (int r = 0; r < KM_RMAX; ++r) {
-                    const int64_t t = dc + lane + 32 * r;
-                    v[u][r] = (pi[u] >= 0 && t < d) ? (double)__ldg(P + (int64_t)pi[u] * d + t) : 0.0;
-                }
-#pragma unroll
-            for (int u = 0; u < KM_SEGB; ++u)
-                if (pi[u] >= 0) {
-#pragma unroll
-                    for (int r = 0; r < KM_RMAX; ++r) g[r] += cj[r] - v[u][r];
-                }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < KM_RMAX; ++r) part[w][lane + 32 * r] = g[r];
-        __syncthreads();
-        if (w == 0) {
-            const double h = two_y * (double)len;
-#pragma unroll
-            for (int r = 0; r < KM_RMAX; ++r) {
-                const int64_t t = dc + lane + 32 * r;
-                double tot = part[0][lane + 32 * r];
-#pragma unroll
-                for (int q = 1; q < KM_SEGW; ++q) tot += part[q][lane + 32 * r];
-                if (t < d) {
-                    const double cb = two_y * tot;
-                    Cbar[j * d + t] = acc ? (T)((double)Cbar[j * d + t] + cb) : (T)cb;
-                    if (H) H[j * d + t] = acc ? (T)((double)H[j * d + t] + h) : (T)h;
-                }
-            }
-        }
-    }
-}
-
 template <class T>
 __global__ void km_cost_final(const double *__restrict__ part, int64_t np, T *__restrict__ cost, int acc) {
     __shared__ double s[256];
@@ -654,21 +468,19 @@ namespace {
 using namespace vjph;
 
 struct KmLayout {
-    size_t cn, part, hist, colsum, start, order, assign, total;
-    int64_t nbA, nbH;
+    size_t cn, part, assign, sort, total;
+    int64_t nbA;
+    BsLayout bs;  // the center accumulator's bin sort (binsort.cuh)
 };
 KmLayout km_layout(int64_t n, int64_t k) {
     KmLayout L{};
     L.nbA = (n + vjpk::KM_BP - 1) / vjpk::KM_BP;
-    L.nbH = (n + vjpk::KM_BH - 1) / vjpk::KM_BH;
+    L.bs = bs_layout(n, k);
     size_t off = 0;
     L.cn = off; off += align256((size_t)k * 8);
     L.part = off; off += align256((size_t)(L.nbA > 0 ? L.nbA : 1) * 8);
-    L.hist = off; off += align256((size_t)(L.nbH > 0 ? L.nbH : 1) * (size_t)k * 4);
-    L.colsum = off; off += align256((size_t)k * 4);
-    L.start = off; off += align256((size_t)(k + 1) * 4);
-    L.order = off; off += align256((size_t)(n > 0 ? n : 1) * 4);
     L.assign = off; off += align256((size_t)(n > 0 ? n : 1) * 4);
+    L.sort = off; off += L.bs.total;
     L.total = off;
     return L;
 }
@@ -680,10 +492,6 @@ vjp_status km_run(int64_t n, int64_t k, int64_t d, const void *P, const void *C,
     unsigned char *w = static_cast<unsigned char *>(ws);
     double *cn = reinterpret_cast<double *>(w + L.cn);
     double *part = reinterpret_cast<double *>(w + L.part);
-    int32_t *hist = reinterpret_cast<int32_t *>(w + L.hist);
-    int32_t *colsum = reinterpret_cast<int32_t *>(w + L.colsum);
-    int32_t *start = reinterpret_cast<int32_t *>(w + L.start);
-    int32_t *order = reinterpret_cast<int32_t *>(w + L.order);
     int32_t *asg = assign ? assign : reinterpret_cast<int32_t *>(w + L.assign);
     const T *Pt = static_cast<const T *>(P);
     const T *Ct = static_cast<const T *>(C);
@@ -716,29 +524,16 @@ vjp_status km_run(int64_t n, int64_t k, int64_t d, const void *P, const void *C,
             cudaFuncSetAttribute(ka, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asm_);
             ka<<<(unsigned)L.nbA, vjpk::KM_NT, asm_, s>>>(Pt, Ct, cn, n, k, d, asg, part);
         }
-        const size_t hsm = (size_t)k * 4;
-        cudaFuncSetAttribute(vjpk::km_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
-        vjpk::km_hist<<<(unsigned)L.nbH, 256, hsm, s>>>(asg, n, k, hist);
-        launches += 2;
-    }
-    vjpk::km_colscan<<<(unsigned)((k + 31) / 32), 1024, 0, s>>>(hist, n > 0 ? L.nbH : 0, k, colsum);
-    vjpk::km_startscan<<<1, 1024, 0, s>>>(colsum, k, start, counts, acc);
-    launches += 2;
-    if (n > 0) {
-        const int wpb = 4;
-        const size_t osm = (size_t)wpb * (size_t)k * 4;
-        cudaFuncSetAttribute(vjpk::km_order, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)osm);
-        vjpk::km_order<<<(unsigned)((L.nbH + wpb - 1) / wpb), 32 * wpb, osm, s>>>(asg, n, k, hist, start, order,
-                                                                               L.nbH);
         ++launches;
     }
-    {
-        // dims per lane per pass: 32 R covers d = 32, 64 in one pass; wider d loops
-        auto ks = d <= 32 ? vjpk::km_segsum<T, 1> : (d <= 64 ? vjpk::km_segsum<T, 2> : vjpk::km_segsum<T, 4>);
-        ks<<<(unsigned)k, 32 * vjpk::KM_SEGW, 0, s>>>(Pt, Ct, order, start, k, d, static_cast<const T *>(cost_bar),
-                                                          static_cast<T *>(Cbar), static_cast<T *>(H), acc);
-    }
-    ++launches;
+    // the return sweep's accumulator: C_bar_j = 2 ybar sum_{p: a(p) = j} (c_j - p)
+    // and H_j = 2 ybar cnt_j — a width-d reduce_by_index(+) of the rows
+    // (c_{a(p)} - p) into k bins, done by the
+    // library's deterministic bin sort + segmented row sums (binsort.cuh),
+    // the same routine as vjp_reduce_by_index(+)'s primal histogram
+    launches += bs_sort<int32_t>(asg, n, k, L.bs, w + L.sort, counts, acc, s);
+    launches += bs_rowsum<T>(Pt, Ct, k, d, 2.0, static_cast<const T *>(cost_bar), L.bs, w + L.sort,
+                             static_cast<T *>(Cbar), static_cast<T *>(H), acc, s);
     if (cost) {
         if (n > 0) {
             vjpk::km_cost_final<T><<<1, 256, 0, s>>>(part, L.nbA, static_cast<T *>(cost), acc);

@@ -22,6 +22,7 @@
 
 #include "common.cuh"
 #include "log2_table.cuh"
+#include "binsort.cuh"
 
 namespace vjpk {
 
@@ -409,7 +410,7 @@ __device__ __forceinline__ void red_max_u64_shared(unsigned long long *a, unsign
 // into the global keys at the end; large m: the global keys in L2.
 template <class T, class I, int OP, bool SMEM>
 __global__ void __launch_bounds__(kBThreads, kBMinBlocks) rbi_ext_a(const I *__restrict__ inds, const T *__restrict__ as,
-                                                       RbiParams P) {
+                                                       T *__restrict__ ab, RbiParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     unsigned long long *hk = reinterpret_cast<unsigned long long *>(smem);
     const bool is_min = OP == VJP_MIN;
@@ -423,7 +424,7 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) rbi_ext_a(const I *__r
     const int64_t R = P.cap / nw;  // this warp's region of the candidate list
     unsigned long long *reg = P.cand + 3 * gw * R;
     int64_t cnt = 0;
-    rbi_stream<T, I>(inds, as, nullptr, P, [&](int64_t b, double x, int64_t gi, bool ok) {
+    rbi_stream<T, I>(inds, as, ab, P, [&](int64_t b, double x, int64_t gi, bool ok) {
         uint64_t k = 0;
         bool cand = false;
         if (ok) {
@@ -914,12 +915,12 @@ vjp_status forward(const I *inds, const T *as, T *ab, RbiParams P, cudaStream_t 
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smk);
             ga = grid_resident(k, work, smk);
             if ((int64_t)ga * (kBThreads / 32) > kMaxWarpsA) ga = (int)(kMaxWarpsA / (kBThreads / 32));
-            k<<<ga, kBThreads, smk, s>>>(inds, as, P);
+            k<<<ga, kBThreads, smk, s>>>(inds, as, ab, P);
         } else {
             auto k = rbi_ext_a<T, I, OP, false>;
             ga = grid_resident(k, work);
             if ((int64_t)ga * (kBThreads / 32) > kMaxWarpsA) ga = (int)(kMaxWarpsA / (kBThreads / 32));
-            k<<<ga, kBThreads, 0, s>>>(inds, as, P);
+            k<<<ga, kBThreads, 0, s>>>(inds, as, ab, P);
         }
         vjph::count_launch();
         rbi_ext_b<T, I, OP><<<grid_resident(rbi_ext_b<T, I, OP>, work), kBThreads, 0, s>>>(inds, as, P,
@@ -929,9 +930,24 @@ vjp_status forward(const I *inds, const T *as, T *ab, RbiParams P, cudaStream_t 
     return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
 }
 
+// deterministic primal sum of the rows (ADD with hs requested): the bin sort
+// + in-order segmented sums of binsort.cuh, when the caller's workspace holds
+// it (vjp_reduce_by_index_hs_workspace_bytes); else atomic adds
+bool add_sorted_ok(int64_t n, int64_t m, size_t ws_bytes) {
+    return m <= vjph::kBsMaxBins && n < ((int64_t)1 << 31) && ws_bytes >= vjph::bs_layout(n, m).total;
+}
+template <class T, class I>
+int add_hist_sorted(const I *inds, const T *as, int64_t n, int64_t m, int64_t w, T *hs, void *ws, cudaStream_t s) {
+    const vjph::BsLayout L = vjph::bs_layout(n, m);
+    unsigned char *wb = static_cast<unsigned char *>(ws);
+    int k = vjph::bs_sort<I>(inds, n, m, L, wb, nullptr, 0, s);
+    k += vjph::bs_rowsum<T>(as, nullptr, m, w, 1.0, nullptr, L, wb, hs, nullptr, 0, s);
+    return k;
+}
+
 template <class T, class I>
 vjp_status run_full(vjp_op op, int64_t n, int64_t m, const void *inds_, const void *as_, const void *hsb_, void *ab_,
-                    void *hs_, int64_t *winners, void *ws, cudaStream_t s, unsigned flags) {
+                    void *hs_, int64_t *winners, void *ws, size_t ws_bytes, cudaStream_t s, unsigned flags) {
     const I *inds = static_cast<const I *>(inds_);
     const T *as = static_cast<const T *>(as_);
     const T *hsb = static_cast<const T *>(hsb_);
@@ -940,8 +956,10 @@ vjp_status run_full(vjp_op op, int64_t n, int64_t m, const void *inds_, const vo
     const int acc = (flags & VJP_ACCUMULATE) ? 1 : 0;
     const int nvec = (int)(16 / sizeof(I));
     if (op == VJP_ADD) {
-        if (hs) {
-            // primal histogram only on request: atomic adds (order-dependent rounding)
+        if (hs && add_sorted_ok(n, m, ws_bytes)) {
+            vjph::count_launch(add_hist_sorted<T, I>(inds, as, n, m, 1, hs, ws, s));
+        } else if (hs) {
+            // primal histogram on request, atomic adds (order-dependent rounding)
             if (cudaMemsetAsync(hs, 0, sizeof(T) * (size_t)m, s) != cudaSuccess) return VJP_ECUDA;
             RbiParams P = params(n, m, 0, ws, 0, 0);
             P.v256 = a32(as);
@@ -954,10 +972,14 @@ vjp_status run_full(vjp_op op, int64_t n, int64_t m, const void *inds_, const vo
         if (winners && cudaMemsetAsync(winners, 0xff, sizeof(int64_t) * (size_t)m, s) != cudaSuccess) return VJP_ECUDA;
         return VJP_OK;
     }
-    // dense MIN/MAX: as_bar = 0 except the winners (a plain memset; the
-    // scatter below overwrites the m winners)
-    if (op != VJP_MUL && !acc && cudaMemsetAsync(ab, 0, sizeof(T) * (size_t)n, s) != cudaSuccess) return VJP_ECUDA;
-    RbiParams P = params(n, m, 0, ws, flags, 0, op != VJP_MUL);
+    // dense MIN/MAX: as_bar = 0 except the winners; the scatter below
+    // overwrites the m winners.  Small m (shared-memory filter, latency bound):
+    // a plain memset first (fusing the stores slowed phase A, DESIGN 7.6);
+    // large m (L2 bound): phase A stores the zeros while it streams the bins
+    const bool fuse_zero = op != VJP_MUL && !acc && (size_t)m * 8 > 128 * 1024;
+    if (op != VJP_MUL && !acc && !fuse_zero && cudaMemsetAsync(ab, 0, sizeof(T) * (size_t)n, s) != cudaSuccess)
+        return VJP_ECUDA;
+    RbiParams P = params(n, m, 0, ws, flags, fuse_zero ? 1 : 0, op != VJP_MUL);
     P.v256 = a32(as) && a32(ab);
     vjp_status st = VJP_OK;
     if (op == VJP_MUL) st = forward<T, I, VJP_MUL>(inds, as, ab, P, s);
@@ -1052,8 +1074,8 @@ int grid_wide(const WideGeo &g) {
 }
 template <class T, class I>
 vjp_status run_wide(vjp_op op, int64_t n, int64_t m, int64_t w, const void *inds_, const void *as_,
-                    const void *hsb_, void *ab_, void *hs_, int64_t *winners, void *ws, cudaStream_t s,
-                    unsigned flags) {
+                    const void *hsb_, void *ab_, void *hs_, int64_t *winners, void *ws, size_t ws_bytes,
+                    cudaStream_t s, unsigned flags) {
     const I *inds = static_cast<const I *>(inds_);
     const T *as = static_cast<const T *>(as_);
     const T *hsb = static_cast<const T *>(hsb_);
@@ -1064,7 +1086,9 @@ vjp_status run_wide(vjp_op op, int64_t n, int64_t m, int64_t w, const void *inds
     const int grid = grid_wide(g);
     const int64_t mw = m * w;
     if (op == VJP_ADD) {
-        if (hs) {
+        if (hs && add_sorted_ok(n, m, ws_bytes)) {
+            vjph::count_launch(add_hist_sorted<T, I>(inds, as, n, m, w, hs, ws, s));
+        } else if (hs) {
             if (cudaMemsetAsync(hs, 0, sizeof(T) * (size_t)mw, s) != cudaSuccess) return VJP_ECUDA;
             rbiw_add_hist<T, I><<<grid, kBThreads, 0, s>>>(inds, as, hs, g);
             vjph::count_launch();
@@ -1143,6 +1167,13 @@ size_t vjp_reduce_by_index_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_t n
     return blayout(m, n, op != VJP_MUL).total;
 }
 
+size_t vjp_reduce_by_index_hs_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_t n, int64_t m, int64_t width) {
+    const size_t base = vjp_reduce_by_index_workspace_bytes(op, dtype, n, m, width);
+    if (op != VJP_ADD || m < 1 || n < 0 || width < 1 || m > vjph::kBsMaxBins || n >= ((int64_t)1 << 31)) return base;
+    const size_t srt = vjph::bs_layout(n, m).total;
+    return srt > base ? srt : base;
+}
+
 vjp_status vjp_reduce_by_index(vjp_op op, vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, int64_t width,
                                const void *inds, const void *as, const void *hs_bar, void *as_bar, void *hs,
                                int64_t *winners, void *ws, size_t ws_bytes, vjp_stream_t stream, unsigned flags) {
@@ -1156,8 +1187,9 @@ vjp_status vjp_reduce_by_index(vjp_op op, vjp_dtype dtype, vjp_itype itype, int6
     if (ws_bytes < need || (need && !ws)) return VJP_EWORKSPACE;
     if (ws && !vjph::aligned16(ws)) return VJP_EALIGN;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    if (width > 1) return RBI_DISPATCH(run_wide, op, n, m, width, inds, as, hs_bar, as_bar, hs, winners, ws, s, flags);
-    return RBI_DISPATCH(run_full, op, n, m, inds, as, hs_bar, as_bar, hs, winners, ws, s, flags);
+    if (width > 1)
+        return RBI_DISPATCH(run_wide, op, n, m, width, inds, as, hs_bar, as_bar, hs, winners, ws, ws_bytes, s, flags);
+    return RBI_DISPATCH(run_full, op, n, m, inds, as, hs_bar, as_bar, hs, winners, ws, ws_bytes, s, flags);
 }
 
 vjp_status vjp_reduce_by_index_partial(vjp_op op, vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m,

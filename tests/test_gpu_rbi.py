@@ -225,3 +225,25 @@ def test_rbi_width_goldens():
             assert win.cpu().tolist() == c["winners"], c["id"]
         if "hs" in c:
             assert hs.cpu().tolist() == c["hs"], c["id"]
+
+
+@pytest.mark.parametrize("width", [1, 3, 64])
+def test_rbi_add_primal_deterministic(width):
+    """the ADD primal histogram (hs) comes from the bin sort + in-order
+    segmented sums (binsort.cuh, the k-means accumulator's routine): identical
+    bits on every call, bit-exact against the oracle on integer-valued rows,
+    out-of-range bins skipped (R4)"""
+    n, m = 200_003, 777
+    inds, a, hb = synth.rbi_wide_inputs(n, m, width, "add")
+    inds[5] = -3
+    inds[9] = m
+    ai = synth.integers(n * width, 71, -1000, 1000).to(torch.float64)
+    d = [t.to(DEV) for t in (inds, a, ai, hb)]
+    h1 = vjp.reduce_by_index("add", d[0], d[1], d[3], want_hs=True, width=width)[1]
+    h2 = vjp.reduce_by_index("add", d[0], d[1], d[3], want_hs=True, width=width)[1]
+    assert torch.equal(h1, h2)
+    ref = oracle.vjp_reduce_by_index("add", inds.numpy(), a.numpy(), hb.numpy(), width=width)[1]
+    assert_close(h1.cpu().numpy(), ref, np.float64, scale=np.full(m * width, n / m), what="primal sum")
+    hi = vjp.reduce_by_index("add", d[0], d[2], d[3], want_hs=True, width=width)[1]
+    refi = oracle.vjp_reduce_by_index("add", inds.numpy(), ai.numpy(), hb.numpy(), width=width)[1]
+    assert np.array_equal(hi.cpu().numpy(), refi)

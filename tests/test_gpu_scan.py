@@ -276,3 +276,23 @@ def test_scan_host_async_pipeline():
         got = p.wait()
         assert got.data_ptr() == out.data_ptr()
         assert torch.equal(got, ref)
+
+
+@pytest.mark.parametrize("op", ["linrec", "mat2"])
+def test_bench_sequence_dist_scan_world1(op):
+    """the exact call sequence bench.py times for config 2 (dist.scan at
+    world = 1: vjp_scan_partial + vjp_scan_finish on a whole-array 'shard',
+    events around the finish, a preallocated out) against the oracle, at a
+    tile-spanning ragged size and twice in a row on the same buffers"""
+    from paper_2202_10297_b200 import dist as vdist
+    n = 3 * (1 << 16) + 123
+    a, yb = make(op, n, np.float64)
+    ref = oracle.vjp_scan(op, yb.numpy(), a.numpy())
+    ad, ybd = a.to(DEV), yb.to(DEV)
+    ab = torch.empty_like(ybd)
+    for _ in range(2):
+        ev = {"finish_start": torch.cuda.Event(enable_timing=True), "finish_end": torch.cuda.Event(enable_timing=True)}
+        vdist.scan(op, ybd, ad, offset=0, global_n=n, out=ab, events=ev)
+        torch.cuda.synchronize()
+        assert ev["finish_start"].elapsed_time(ev["finish_end"]) > 0
+        assert_close(ab.cpu().numpy(), ref, np.float64, what=f"bench sequence {op}")
