@@ -9,6 +9,7 @@
 #include <cstdlib>
 
 #include "scan_blocklb.cuh"
+#include "scan_add1p.cuh"
 
 namespace vjph {
 
@@ -76,7 +77,8 @@ struct ScanImpl {
         size_t counters, flags1, flags2, memset_bytes, p1agg, p1inc, p2agg, p2inc, partial;
         int64_t ntiles_c;
         size_t tileF, tileP, chunkRec, counter_c, roundRec, arrive, lbFlags, lbAgg, lbInc, lbTileF, lbTileP, lbPark,
-            total;
+            p1Ctr, p1Agg, p1Inc, p1Grp, p1End, total;
+        int64_t p1Tiles;
     };
     static Layout layout(int64_t n) {
         Layout L{};
@@ -108,6 +110,14 @@ struct ScanImpl {
         L.lbTileF = off; off += align256((size_t)ntl * W * 8);
         L.lbTileP = off; off += align256((size_t)ntl * W * 8);
         L.lbPark = off; off += align256((size_t)NTL_MIN * (W + MD) * 8);  // the last tile's parked rows
+        // one-pass scan(+) (scan_add1p.cuh): ticket + group counters | records
+        L.p1Tiles = n > 0 ? (n + P1_TE - 1) / P1_TE : 0;
+        const int64_t p1g = (L.p1Tiles + 31) / 32;
+        L.p1Ctr = off; off += align256(256 + (size_t)p1g * 4);
+        L.p1Agg = off; off += align256((size_t)L.p1Tiles * 16);
+        L.p1Inc = off; off += align256((size_t)L.p1Tiles * 16);
+        L.p1Grp = off; off += align256((size_t)p1g * 16);
+        L.p1End = off;
         L.total = off;
         return L;
     }
@@ -438,6 +448,47 @@ struct ScanImpl {
             return s2 == VJP_OK ? finish_c(c) : s2;
         }
         return st;
+    }
+
+    // ---------------- one-pass scan(+) with two-level look-back (scan_add1p.cuh) ----------------
+    static constexpr int P1_RPT = 2;  // rows per thread: 64 KB tiles
+    static constexpr int64_t P1_TE = (int64_t)vjpk::k1pData * P1_RPT * 128 / (int64_t)sizeof(T);
+    static bool use_1p(const ScanCall &c) {
+        if constexpr (!std::is_same<Op, vjpk::OpAdd>::value) {
+            return false;
+        } else {
+            if (c.world != 1 || c.ys || c.cyc) return false;
+            if (c.flags & (VJP_SCAN_LOOKBACK | VJP_SCAN_CHUNKED | VJP_SCAN_SWEEP | VJP_SCAN_BLOCKLB | VJP_ACCUMULATE))
+                return false;  // ACCUMULATE (as_bar read as well) keeps the sweep / chunked kernels
+            // 1-D bulk copies: 16-byte aligned arrays (the ABI's requirement)
+            return true;
+        }
+    }
+    static vjp_status launch_1p(const ScanCall &c) {
+        Layout L = layout(c.n);
+        unsigned char *ws = static_cast<unsigned char *>(c.ws);
+        if (cudaMemsetAsync(ws + L.p1Ctr, 0, L.p1End - L.p1Ctr, c.stream) != cudaSuccess) return VJP_ECUDA;
+        vjpk::Add1pParams P{};
+        P.n = c.n;
+        P.ntiles = L.p1Tiles;
+        P.ys_bar = c.ys_bar;
+        P.as_bar = c.as_bar;
+        P.ticket = reinterpret_cast<uint32_t *>(ws + L.p1Ctr);
+        P.gcount = reinterpret_cast<uint32_t *>(ws + L.p1Ctr + 256);
+        P.agg = reinterpret_cast<double2 *>(ws + L.p1Agg);
+        P.inc = reinterpret_cast<double2 *>(ws + L.p1Inc);
+        P.grp = reinterpret_cast<double2 *>(ws + L.p1Grp);
+        constexpr size_t sm = 1024 + (size_t)vjpk::k1pData * P1_RPT * 128;
+        auto k = vjpk::scan_add_1p<T, P1_RPT>;
+        set_smem(k, sm);
+        const int64_t rows = c.n * (int64_t)sizeof(T) / vjpk::kRowBytes;  // full 128-byte rows
+        CUtensorMap mi, mo;
+        if (!make_row_tmap(&mi, c.ys_bar, rows, sizeof(T) == 8, 256) ||
+            !make_row_tmap(&mo, c.as_bar, rows, sizeof(T) == 8, 256))
+            return VJP_ECUDA;
+        k<<<(unsigned)L.p1Tiles, vjpk::k1pData + 32, sm, c.stream>>>(mi, mo, P);
+        count_launch();
+        return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
     }
 
     // ---------------- block-cyclic multi-GPU sweep (scan_sweep.cuh) ----------------
@@ -796,6 +847,7 @@ struct ScanImpl {
     }
 
     static vjp_status partial(const ScanCall &c) {
+        if (use_1p(c)) return VJP_OK;             // one pass, in finish
         if (use_lb(c)) return phase_lb(c, true);  // the `as`-only forward pre-pass K_F (nothing for scan(+))
         if constexpr (Op::kRevNeedsRs) {
             if (use_rs_chunked(c)) return partial_rs(c);
@@ -822,6 +874,7 @@ struct ScanImpl {
     }
 
     static vjp_status finish(const ScanCall &c) {
+        if (use_1p(c)) return launch_1p(c);
         if (use_lb(c)) return phase_lb(c, false);
         if constexpr (Op::kRevNeedsRs) {
             if (use_rs_chunked(c)) return finish_rs(c);

@@ -1,5 +1,6 @@
-"""Tuning helper: scan(+) at 2^30 for f32 / f64 on the sweep and the chunked
-kernels (CUDA events, median of 10 after 3 warm-ups)."""
+"""Tuning helper: scan(+) for f32 / f64 on the default path (one pass, two-level
+look-back), the sweep and the chunked kernels (CUDA events, median of 10
+after 3 warm-ups).  python tools/time_scan_paths.py [log2 n ...]"""
 import os
 import statistics
 import sys
@@ -10,11 +11,13 @@ import torch  # noqa: E402
 import paper_2202_10297_b200 as vjp  # noqa: E402
 import synth  # noqa: E402
 
-n = 1 << 30
-for dt in (torch.float32, torch.float64):
+import json
+peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"] if os.path.exists("MEASURED_PEAKS.json") else 6543.4
+for n in [1 << int(x) for x in (sys.argv[1:] or ["30"])]:
+  for dt in (torch.float32, torch.float64):
     yb = synth.scan_add_seed(n, device="cuda").to(dt)
     out = torch.empty_like(yb)
-    for label, kw in (("sweep", {"sweep": True}), ("chunked", {"chunked": True})):
+    for label, kw in (("default", {}), ("sweep", {"sweep": True}), ("chunked", {"chunked": True})):
         for _ in range(3):
             vjp.scan("add", yb, out=out, **kw)
         ts = []
@@ -25,5 +28,6 @@ for dt in (torch.float32, torch.float64):
             e1.record()
             e1.synchronize()
             ts.append(e0.elapsed_time(e1))
-        print(f"{str(dt):14s} {label:8s} {statistics.median(ts):.3f} ms", flush=True)
+        t = statistics.median(ts)
+        print(f"n=2^{n.bit_length() - 1} {str(dt):14s} {label:8s} {t:.3f} ms  frac {2 * yb.element_size() * n / (t * 1e-3) / 1e9 / peak:.3f}", flush=True)
     del yb, out
