@@ -478,15 +478,17 @@ struct ScanImpl {
         P.agg = reinterpret_cast<double2 *>(ws + L.p1Agg);
         P.inc = reinterpret_cast<double2 *>(ws + L.p1Inc);
         P.grp = reinterpret_cast<double2 *>(ws + L.p1Grp);
-        constexpr size_t sm = 1024 + (size_t)vjpk::k1pData * P1_RPT * 128;
-        auto k = vjpk::scan_add_1p<T, P1_RPT>;
-        set_smem(k, sm);
         const int64_t rows = c.n * (int64_t)sizeof(T) / vjpk::kRowBytes;  // full 128-byte rows
         CUtensorMap mi, mo;
         if (!make_row_tmap(&mi, c.ys_bar, rows, sizeof(T) == 8, 256) ||
             !make_row_tmap(&mo, c.as_bar, rows, sizeof(T) == 8, 256))
             return VJP_ECUDA;
-        k<<<(unsigned)L.p1Tiles, vjpk::k1pData + 32, sm, c.stream>>>(mi, mo, P);
+        constexpr size_t sm = 1024 + (size_t)vjpk::k1pData * P1_RPT * 128;
+        auto k = vjpk::scan_add_1p<T, P1_RPT>;
+        set_smem(k, sm);
+        vjpk::Add1pParams Q = P;
+        Q.ntiles = (c.n + P1_TE - 1) / P1_TE;
+        k<<<(unsigned)Q.ntiles, vjpk::k1pData + 32, sm, c.stream>>>(mi, mo, Q);
         count_launch();
         return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
     }
