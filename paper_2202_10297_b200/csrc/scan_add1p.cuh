@@ -4,7 +4,7 @@
 // 8 B f32: the method bytes).  The default for scan(+) on one GPU without
 // ys / ACCUMULATE (DESIGN 7.1d).
 //
-// Tiles of 512 rows x 128 B (64 KB) staged in shared memory by TMA.  CTAs
+// Tiles of 768 rows x 128 B (96 KB) staged in shared memory by TMA (2 CTAs per SM).  CTAs
 // take tickets in start order; ticket k is the k-th tile from the RIGHT (the
 // return sweep runs right to left).  A tile publishes its
 // aggregate (AGG record, one 16-byte store = flag + value) as soon as it has
@@ -144,7 +144,7 @@ __device__ __forceinline__ void bar_named(int id, int count) {
 }
 
 // 8 data warps + 1 look-back warp that computes the exclusive sum WHILE the
-// tile streams in.  The tile (256 threads x RPT rows of 128 B; RPT = 2: 64 KB)
+// tile streams in.  The tile (256 threads x RPT rows of 128 B; RPT = 3: 96 KB)
 // moves global -> shared -> global by 2-D TMA with the 128B swizzle (one box
 // of 256 rows per TMA instruction, mbarrier completion), so a CTA holds no
 // tile data in registers while its look-back runs; thread t owns rows

@@ -451,7 +451,7 @@ struct ScanImpl {
     }
 
     // ---------------- one-pass scan(+) with two-level look-back (scan_add1p.cuh) ----------------
-    static constexpr int P1_RPT = 2;  // rows per thread: 64 KB tiles
+    static constexpr int P1_RPT = 3;  // rows per thread: 96 KB tiles
     static constexpr int64_t P1_TE = (int64_t)vjpk::k1pData * P1_RPT * 128 / (int64_t)sizeof(T);
     static bool use_1p(const ScanCall &c) {
         if constexpr (!std::is_same<Op, vjpk::OpAdd>::value) {
