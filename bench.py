@@ -638,6 +638,45 @@ def run_extra(args):
         ybm = torch.tensor([1.0, 0.5, -0.5, 2.0], dtype=torch.float64, device=dev)
         cases.append(("general reduce MAT2 f64 n=2^26", N26, 96 * N26,
                       lambda am=am, om=om, ybm=ybm: vjp.reduce("mat2", am, ybm, out=om)))
+    if w == "call":
+        # one vjp call from the flags (method bytes as in SURVEY 8d / DESIGN 7)
+        n = args.n or (1 << 28)
+        td = torch.float64 if args.dtype == "f64" else torch.float32
+        es = 8 if args.dtype == "f64" else 4
+        width = {"linrec": 2, "mat2": 4}.get(args.op, 1)
+        if args.kind == "scan":
+            gen = {"linrec": synth.linrec_inputs, "mat2": synth.mat2_inputs}
+            if args.op in gen:
+                a, yb = gen[args.op](n, dtype=td, device=dev)
+            elif args.op == "add":
+                a, yb = None, synth.scan_add_seed(n, dtype=td, device=dev)
+            elif args.op in ("min", "max"):
+                a, yb = synth.min_inputs(n, dtype=td, device=dev), synth.uniform(n, 10, dtype=td, device=dev)
+            else:
+                a = (1.0 + (synth.uniform(n, 7, device=dev) - 0.5) * 2.0 ** -6).to(td)
+                yb = synth.uniform(n, 8, dtype=td, device=dev)
+            out = torch.empty_like(yb)
+            nb = (2 if args.op == "add" else 4) * width * es
+            cases.append((f"scan {args.op.upper()} {args.dtype} n={n}", n, nb * n,
+                          lambda: vjp.scan(args.op, yb, a, out=out)))
+        elif args.kind == "reduce":
+            if args.op == "mul":
+                a = synth.mul_inputs(n, dtype=td, device=dev)
+            elif args.op in ("min", "max"):
+                a = synth.min_inputs(n, dtype=td, device=dev)
+            else:
+                a = synth.uniform(n * width, 5, dtype=td, device=dev)
+            out = torch.empty_like(a)
+            nb = {"add": 1, "mul": 3, "min": 2, "max": 2}.get(args.op, 3) * width * es
+            ybar = 1.0 if width == 1 else torch.ones(width, dtype=td, device=dev)
+            cases.append((f"reduce {args.op.upper()} {args.dtype} n={n}", n, nb * n,
+                          lambda: vjp.reduce(args.op, a, ybar, out=out)))
+        else:
+            inds, a, hb = synth.rbi_inputs(n, args.m, args.op, dtype=td, device=dev)
+            out = torch.empty(n, dtype=td, device=dev)
+            nb = {"add": 4 + es, "mul": 4 + 3 * es, "max": 4 + 2 * es, "min": 4 + 2 * es}[args.op]
+            cases.append((f"rbi {args.op.upper()} {args.dtype} n={n} m={args.m}", n, nb * n,
+                          lambda: vjp.reduce_by_index(args.op, inds, a, hb, out=out)))
     if w in ("kmeans", "all"):
         # config 5: n = 10^6 points, d = 64, k = 1024, f64 (one call: forward
         # distance/argmin on the FP64 tensor pipe + the return sweep)
@@ -660,11 +699,22 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-targets", action="store_true", help="skip the north_star target kernels (1 GPU)")
     ap.add_argument("--workload", default="config2",
-                    choices=["config2", "scan_add", "scan_linrec30", "reduce", "rbi", "kmeans", "batched", "all"],
-                    help="config2 = the headline line; the others print per-call extra lines")
+                    choices=["config2", "scan_add", "scan_linrec30", "reduce", "rbi", "kmeans", "batched", "call",
+                             "all"],
+                    help="config2 = the headline line; the others print per-call extra lines; call = one vjp "
+                         "call chosen by --kind/--op/--dtype/--n/--m")
+    ap.add_argument("--kind", default="scan", choices=["scan", "reduce", "rbi"], help="--workload call: combinator")
+    ap.add_argument("--op", default="add", choices=["add", "mul", "min", "max", "linrec", "mat2"],
+                    help="--workload call: operator")
+    ap.add_argument("--dtype", default="f64", choices=["f32", "f64"], help="--workload call: value dtype")
+    ap.add_argument("--m", type=int, default=1000, help="--workload call, rbi: bins")
+    ap.add_argument("--seed", type=int, default=2202, help="synthetic-input seed (synth.set_seed)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.seed != 2202:
+        import synth
+        synth.set_seed(args.seed)
     if args.impl == "reference":
         return run_reference(args)
     if args.workload != "config2":

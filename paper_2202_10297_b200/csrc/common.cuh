@@ -3,6 +3,7 @@
 // release/acquire status flags for decoupled look-back, launch bookkeeping.
 #pragma once
 
+#include <nvtx3/nvToolsExt.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -109,6 +110,13 @@ __device__ __forceinline__ T shfl_idx_t(T v, int l) { return __shfl_sync(0xfffff
 // host helpers (vjp_host.cu)
 // ---------------------------------------------------------------------------
 namespace vjph {
+// NVTX range around every C-ABI call (header-only NVTX3: a no-op unless a
+// tool — nsys, ncu --nvtx — is attached), named after the entry point
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+#define VJP_NVTX(name) vjph::NvtxRange vjp_nvtx_range_(name)
 // 2-D tensor map over `bytes_full` bytes viewed as rows of 128 bytes; box =
 // 128 B x kThreads rows, 128B swizzle.  Returns false if it could not be built.
 bool make_row_tmap(CUtensorMap *map, const void *base, int64_t rows, bool f64, int box_rows = vjpk::kThreads);

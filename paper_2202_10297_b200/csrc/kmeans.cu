@@ -559,6 +559,7 @@ size_t vjp_kmeans_workspace_bytes(vjp_dtype dtype, int64_t n, int64_t k, int64_t
 vjp_status vjp_kmeans(vjp_dtype dtype, int64_t n, int64_t k, int64_t d, const void *points, const void *centers,
                       const void *cost_bar, void *centers_bar, void *hess_diag, int32_t *assign, int64_t *counts,
                       void *cost, void *ws, size_t ws_bytes, vjp_stream_t stream, unsigned flags) {
+    VJP_NVTX("vjp_kmeans");
     if (dtype != VJP_F32 && dtype != VJP_F64) return VJP_EINVAL;
     if (n < 0 || k < 1 || d < 1 || n >= ((int64_t)1 << 31) || k > kKmMaxK) return k > kKmMaxK ? VJP_EUNSUPPORTED : VJP_EINVAL;
     if ((n > 0 && !points) || !centers || !cost_bar || !centers_bar) return VJP_EINVAL;

@@ -1177,6 +1177,7 @@ size_t vjp_reduce_by_index_hs_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_
 vjp_status vjp_reduce_by_index(vjp_op op, vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, int64_t width,
                                const void *inds, const void *as, const void *hs_bar, void *as_bar, void *hs,
                                int64_t *winners, void *ws, size_t ws_bytes, vjp_stream_t stream, unsigned flags) {
+    VJP_NVTX("vjp_reduce_by_index");
     if (width < 1) return VJP_EINVAL;
     vjp_status st = common_check(op, dtype, itype, n, m, inds, as, hs_bar);
     if (st != VJP_OK || n == 0) return st;
@@ -1196,6 +1197,7 @@ vjp_status vjp_reduce_by_index_partial(vjp_op op, vjp_dtype dtype, vjp_itype ity
                                        const void *inds, const void *as, void *ws, size_t ws_bytes,
                                        const vjp_shard *shard, double *bin_val, int64_t *bin_aux,
                                        vjp_stream_t stream) {
+    VJP_NVTX("vjp_reduce_by_index_partial");
     if (!shard) return VJP_EINVAL;
     if (op == VJP_ADD) return op_ok(op) ? VJP_OK : VJP_EINVAL;
     vjp_status st = common_check(op, dtype, itype, n, m, inds, as, inds);
@@ -1228,6 +1230,7 @@ vjp_status vjp_reduce_by_index_finish(vjp_op op, vjp_dtype dtype, vjp_itype ityp
                                       const void *inds, const void *as, const void *hs_bar, void *as_bar,
                                       const double *bin_val, const int64_t *bin_aux, void *ws, size_t ws_bytes,
                                       const vjp_shard *shard, vjp_stream_t stream, unsigned flags) {
+    VJP_NVTX("vjp_reduce_by_index_finish");
     if (!shard) return VJP_EINVAL;
     vjp_status st = common_check(op, dtype, itype, n, m, inds, as, hs_bar);
     if (st != VJP_OK || n == 0) return st;

@@ -357,6 +357,7 @@ size_t vjp_reduce_by_index_general_workspace_bytes(vjp_op op, vjp_dtype dtype, i
 vjp_status vjp_reduce_by_index_general(vjp_op op, vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m,
                                        const void *inds, const void *as, const void *hs_bar, void *as_bar, void *ws,
                                        size_t ws_bytes, vjp_stream_t stream, unsigned flags) {
+    VJP_NVTX("vjp_reduce_by_index_general");
     if (op == VJP_LINREC || op == VJP_MAT2) return VJP_EUNSUPPORTED;
     if (op != VJP_MUL) return VJP_EUNSUPPORTED;  // ADD / MIN / MAX: the special cases are the rule
     if ((dtype != VJP_F32 && dtype != VJP_F64) || (itype != VJP_I32 && itype != VJP_I64)) return VJP_EINVAL;

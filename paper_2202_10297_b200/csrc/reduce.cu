@@ -452,6 +452,7 @@ size_t vjp_reduce_partial_bytes(void) { return sizeof(RRec); }
 
 vjp_status vjp_reduce(vjp_op op, vjp_dtype dtype, int64_t n, const void *as, const void *y_bar, void *as_bar,
                       void *y, int64_t *arg, void *ws, size_t ws_bytes, vjp_stream_t stream, unsigned flags) {
+    VJP_NVTX("vjp_reduce");
     if (op == VJP_LINREC || op == VJP_MAT2) {  // the paper's general rule
         if (arg && n > 0 && cudaMemsetAsync(arg, 0xff, 8, reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess)
             return VJP_ECUDA;  // -1: no index for the general rule
@@ -485,6 +486,7 @@ vjp_status vjp_reduce(vjp_op op, vjp_dtype dtype, int64_t n, const void *as, con
 
 vjp_status vjp_reduce_partial(vjp_op op, vjp_dtype dtype, int64_t n, const void *as, void *ws, size_t ws_bytes,
                               const vjp_shard *shard, void *partial, vjp_stream_t stream) {
+    VJP_NVTX("vjp_reduce_partial");
     if (!shard || !partial || n < 0) return VJP_EINVAL;
     vjp_status st = check(op, dtype, n, as, ws, ws_bytes);
     if (st != VJP_OK) return st;
@@ -508,6 +510,7 @@ vjp_status vjp_reduce_partial(vjp_op op, vjp_dtype dtype, int64_t n, const void 
 vjp_status vjp_reduce_finish(vjp_op op, vjp_dtype dtype, int64_t n, const void *as, const void *y_bar, void *as_bar,
                              void *y, int64_t *arg, void *ws, size_t ws_bytes, const vjp_shard *shard,
                              const void *gathered, vjp_stream_t stream, unsigned flags) {
+    VJP_NVTX("vjp_reduce_finish");
     if (!shard || !gathered || n < 0 || shard->world < 1) return VJP_EINVAL;
     vjp_status st = check(op, dtype, n, as, ws, ws_bytes);
     if (st != VJP_OK) return st;

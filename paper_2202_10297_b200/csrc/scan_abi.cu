@@ -144,6 +144,7 @@ size_t vjp_scan_partial_bytes(vjp_op op, vjp_dtype dtype) {
 
 vjp_status vjp_scan(vjp_op op, vjp_dtype dtype, int64_t n, const void *as, const void *ys_bar, void *as_bar,
                     void *ys, void *ws, size_t ws_bytes, vjp_stream_t stream, unsigned flags) {
+    VJP_NVTX("vjp_scan");
     ScanCall c = make_call(op, dtype, n, as, ys_bar, as_bar, ys, ws, ws_bytes, stream, flags, nullptr);
     vjp_status s = check(c, true);
     if (s != VJP_OK || n == 0) return s;
@@ -156,6 +157,7 @@ vjp_status vjp_scan(vjp_op op, vjp_dtype dtype, int64_t n, const void *as, const
 vjp_status vjp_scan_partial(vjp_op op, vjp_dtype dtype, int64_t n, const void *as, const void *ys_bar, void *ws,
                             size_t ws_bytes, const vjp_shard *shard, void *partial, vjp_stream_t stream,
                             unsigned flags) {
+    VJP_NVTX("vjp_scan_partial");
     if (!shard_ok(shard, n)) return VJP_EINVAL;
     ScanCall c = make_call(op, dtype, n, as, ys_bar, nullptr, nullptr, ws, ws_bytes, stream, flags, shard);
     c.partial = partial;
@@ -174,6 +176,7 @@ vjp_status vjp_scan_partial(vjp_op op, vjp_dtype dtype, int64_t n, const void *a
 vjp_status vjp_scan_partial2(vjp_op op, vjp_dtype dtype, int64_t n, const void *as, const void *ys_bar, void *ws,
                              size_t ws_bytes, const vjp_shard *shard, const void *gathered1, void *partial2,
                              vjp_stream_t stream, unsigned flags) {
+    VJP_NVTX("vjp_scan_partial2");
     if (op != VJP_MIN && op != VJP_MAX) return VJP_EUNSUPPORTED;
     if (!shard_ok(shard, n) || !shard || shard->world < 2) return VJP_EINVAL;
     ScanCall c = make_call(op, dtype, n, as, ys_bar, nullptr, nullptr, ws, ws_bytes, stream, flags, shard);
@@ -189,6 +192,7 @@ vjp_status vjp_scan_partial2(vjp_op op, vjp_dtype dtype, int64_t n, const void *
 vjp_status vjp_scan_finish(vjp_op op, vjp_dtype dtype, int64_t n, const void *as, const void *ys_bar, void *as_bar,
                            void *ys, void *ws, size_t ws_bytes, const vjp_shard *shard, const void *gathered,
                            vjp_stream_t stream, unsigned flags) {
+    VJP_NVTX("vjp_scan_finish");
     if (!shard_ok(shard, n)) return VJP_EINVAL;
     ScanCall c = make_call(op, dtype, n, as, ys_bar, as_bar, ys, ws, ws_bytes, stream, flags, shard);
     c.gathered = gathered;
@@ -283,6 +287,7 @@ size_t vjp_scan_cyclic_fwd_bytes(vjp_op op, vjp_dtype dtype, const vjp_cyclic *c
 
 vjp_status vjp_scan_cyclic_forward(vjp_op op, vjp_dtype dtype, int64_t n_local, const void *as, void *ws,
                                    size_t ws_bytes, const vjp_cyclic *cy, void *sbagg, vjp_stream_t stream) {
+    VJP_NVTX("vjp_scan_cyclic_forward");
     if (!cyc_ok(op, dtype, cy)) return VJP_EINVAL;
     if (op == VJP_MIN || op == VJP_MAX) return VJP_EUNSUPPORTED;
     if (n_local != vjp_scan_cyclic_local_n(cy)) return VJP_EINVAL;
@@ -300,6 +305,7 @@ vjp_status vjp_scan_cyclic_forward(vjp_op op, vjp_dtype dtype, int64_t n_local, 
 vjp_status vjp_scan_cyclic(vjp_op op, vjp_dtype dtype, int64_t n_local, const void *as, const void *ys_bar,
                            void *as_bar, void *ws, size_t ws_bytes, const vjp_cyclic *cy, const void *gathered,
                            vjp_stream_t stream, unsigned flags) {
+    VJP_NVTX("vjp_scan_cyclic");
     if (!cyc_ok(op, dtype, cy)) return VJP_EINVAL;
     if (op == VJP_MIN || op == VJP_MAX) return VJP_EUNSUPPORTED;
     if (n_local != vjp_scan_cyclic_local_n(cy)) return VJP_EINVAL;

@@ -368,6 +368,7 @@ size_t vjp_scan_batched_workspace_bytes(vjp_op op, vjp_dtype dtype, int64_t n, i
 vjp_status vjp_scan_batched(vjp_op op, vjp_dtype dtype, int64_t n, int64_t width, const void *as,
                             const void *ys_bar, void *as_bar, void *ws, size_t ws_bytes, vjp_stream_t stream,
                             unsigned flags) {
+    VJP_NVTX("vjp_scan_batched");
     if ((dtype != VJP_F32 && dtype != VJP_F64) || n < 0 || width < 1) return VJP_EINVAL;
     if (op < VJP_ADD || op > VJP_MAT2) return VJP_EINVAL;
     if (n == 0) return VJP_OK;

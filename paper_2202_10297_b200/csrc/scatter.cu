@@ -139,6 +139,7 @@ size_t vjp_scatter_workspace_bytes(vjp_dtype dtype, int64_t n, int64_t m) {
 vjp_status vjp_scatter(vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, int64_t width, const void *is,
                        const void *ys_bar, void *xs_bar, void *vs_bar, void *ws, size_t ws_bytes, vjp_stream_t stream,
                        unsigned flags) {
+    VJP_NVTX("vjp_scatter");
     if ((dtype != VJP_F32 && dtype != VJP_F64) || (itype != VJP_I32 && itype != VJP_I64)) return VJP_EINVAL;
     if (n < 0 || m < 0 || width < 1) return VJP_EINVAL;
     if ((m > 0 && (!is || !vs_bar)) || (n > 0 && (!ys_bar || !xs_bar))) return VJP_EINVAL;
@@ -168,6 +169,7 @@ vjp_status vjp_scatter(vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, i
 vjp_status vjp_scatter_shard(vjp_dtype dtype, vjp_itype itype, int64_t n_local, int64_t m, int64_t width,
                              const void *is, const void *ys_bar, void *xs_bar, void *vs_bar_partial,
                              const vjp_shard *shard, vjp_stream_t stream) {
+    VJP_NVTX("vjp_scatter_shard");
     if (!shard || shard->world < 1 || shard->global_offset < 0 || n_local < 0 ||
         shard->global_offset + n_local > shard->global_n)
         return VJP_EINVAL;
@@ -196,6 +198,7 @@ vjp_status vjp_scatter_shard(vjp_dtype dtype, vjp_itype itype, int64_t n_local, 
 vjp_status vjp_scatter_forward(vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, int64_t width,
                                const void *is, const void *vs, void *xs, void *xs_saved, void *ws, size_t ws_bytes,
                                vjp_stream_t stream, unsigned flags) {
+    VJP_NVTX("vjp_scatter_forward");
     if ((dtype != VJP_F32 && dtype != VJP_F64) || (itype != VJP_I32 && itype != VJP_I64)) return VJP_EINVAL;
     if (n < 0 || m < 0 || width < 1 || (flags & ~(unsigned)VJP_CHECK_INDICES)) return VJP_EINVAL;
     if (m > 0 && (!is || !vs || !xs_saved || (n > 0 && !xs))) return VJP_EINVAL;
@@ -214,6 +217,7 @@ vjp_status vjp_scatter_forward(vjp_dtype dtype, vjp_itype itype, int64_t n, int6
 
 vjp_status vjp_scatter_restore(vjp_dtype dtype, vjp_itype itype, int64_t n, int64_t m, int64_t width,
                                const void *is, const void *xs_saved, void *ys, vjp_stream_t stream) {
+    VJP_NVTX("vjp_scatter_restore");
     if ((dtype != VJP_F32 && dtype != VJP_F64) || (itype != VJP_I32 && itype != VJP_I64)) return VJP_EINVAL;
     if (n < 0 || m < 0 || width < 1) return VJP_EINVAL;
     if (m > 0 && (!is || !xs_saved || (n > 0 && !ys))) return VJP_EINVAL;

@@ -35,10 +35,19 @@ def _srl(x: torch.Tensor, k: int) -> torch.Tensor:
     return (x >> k) & ((1 << (64 - k)) - 1)
 
 
-def bits(n: int, stream: int, *, offset: int = 0, seed: int = SEED, device="cpu",
+_seed = [SEED]
+
+
+def set_seed(seed: int) -> None:
+    """change the seed of every generator below (default SEED = 2202); the
+    values stay a pure function of (seed, stream, global index)"""
+    _seed[0] = int(seed)
+
+
+def bits(n: int, stream: int, *, offset: int = 0, seed: int | None = None, device="cpu",
          chunk: int = 1 << 25) -> torch.Tensor:
     """splitmix64(base + (offset + i + 1) * golden) for i in [0, n) as int64 bits."""
-    base = _s64(seed * 0x2545F4914F6CDD1D + stream * _KS)
+    base = _s64((_seed[0] if seed is None else seed) * 0x2545F4914F6CDD1D + stream * _KS)
     out = torch.empty(n, dtype=torch.int64, device=device)
     for s in range(0, n, chunk):
         e = min(n, s + chunk)
