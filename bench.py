@@ -548,7 +548,7 @@ def run_extra(args):
     if w in ("scan_add", "all"):
         yb = synth.scan_add_seed(N30, device=dev)
         out = torch.empty_like(yb)
-        cases.append(("scan ADD f64 n=2^30 (target; default = one-read sweep)", N30, 16 * N30,
+        cases.append(("scan ADD f64 n=2^30 (target; default = one pass, two-level look-back)", N30, 16 * N30,
                       lambda yb=yb, out=out: vjp.scan("add", yb, out=out)))
         cases.append(("scan ADD f64 n=2^30 chunked kernels (24 B moved)", N30, 16 * N30,
                       lambda yb=yb, out=out: vjp.scan("add", yb, out=out, chunked=True)))
