@@ -520,6 +520,22 @@ __global__ void rbi_mul_prep(const T *__restrict__ hs_bar, const double *__restr
     }
 }
 
+// q / a without the IEEE division's subroutine: reciprocal estimate, two
+// Newton steps, the product and one residual correction (within 1 ulp of the
+// correctly rounded quotient); a outside [2^-1000, 2^1000] (where the
+// estimate's flush-to-zero or the reciprocal's range matter) takes the IEEE
+// division
+__device__ __forceinline__ double div_fast(double q, double a) {
+    const double aa = fabs(a);
+    if (!(aa > 0x1p-1000 && aa < 0x1p1000)) return q / a;
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+    r = fma(r, fma(-a, r, 1.0), r);
+    r = fma(r, fma(-a, r, 1.0), r);
+    const double y = q * r;
+    return fma(r, fma(-a, y, q), y);
+}
+
 // ADD (gather) and MUL (three cases) return map; lane-contiguous 4-element
 // groups, two slabs per iteration for 8 independent gathers in flight per lane
 template <class T, class I, int OP>
@@ -538,7 +554,7 @@ __device__ __forceinline__ void rbi_bwd_map_body(const I *__restrict__ inds, con
         const int64_t z = (int64_t)__double_as_longlong(k.y);
         if (z == 0) {
             touch = true;
-            return k.x / a;  // hs_bar_b * y_b / a_i
+            return div_fast(k.x, a);  // hs_bar_b * y_b / a_i
         }
         touch = (z == 1 && a == 0.0);  // P:1048-1053 per bin
         return touch ? k.x : 0.0;
