@@ -98,9 +98,12 @@ enum {
                                     kernels (MIN/MAX always use look-back) */
     VJP_SCAN_SWEEP = 1u << 17,    /* single GPU: the one-read L2-round sweep (one persistent
                                     kernel, as/ys_bar read from HBM once, each round re-read
-                                    from L2) for any of ADD/MUL/LINREC/MAT2; it is already the
-                                    default for f64 ADD without ys */
-    VJP_SCAN_CHUNKED = 1u << 18,  /* tuning/testing: force the two chunked kernels */
+                                    from L2) for any of ADD/MUL/LINREC/MAT2; the default for
+                                    f64 ADD with ACCUMULATE.  The default for
+                                    f64/f32 ADD without ys / ACCUMULATE is the one-pass kernel
+                                    with a two-level decoupled look-back */
+    VJP_SCAN_CHUNKED = 1u << 18,  /* tuning/testing: force the two chunked kernels (the default for
+                                    MUL/LINREC/MAT2, and for ADD with ys or on several GPUs) */
     VJP_SCAN_BLOCKLB = 1u << 19   /* tuning/testing: force the one-read block look-back
                                     (single GPU, no ACCUMULATE; opt-in: measured slower than
                                     the chunked kernels) */

@@ -249,6 +249,39 @@ __device__ __forceinline__ void log2tab_load(Log2Tab &t) {
     }
 }
 __device__ __constant__ double kLn1pP[5] = {-1.0 / 6.0, 1.0 / 5.0, -1.0 / 4.0, 1.0 / 3.0, -1.0 / 2.0};
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+// the same code with the table addressed through a 32-bit shared-window
+// address computed once per thread (the hot loop of the small-m histogram)
+__device__ __forceinline__ unsigned long long mul_code_s(double x, uint32_t tb) {
+    long long b = __double_as_longlong(x) & 0x7fffffffffffffffll;
+    int e = (int)(b >> 52);
+    if (e == 0) {  // subnormal
+        b = __double_as_longlong(__longlong_as_double(b) * 0x1p54);
+        e = (int)(b >> 52) - 54;
+    }
+    e -= 1023;
+    const uint32_t k8 = (uint32_t)(b >> 42) & (127u << 3);  // 8 * (top 7 fraction bits)
+    const double m = __longlong_as_double((b & 0x000fffffffffffffll) | 0x3ff0000000000000ll);
+    const double r = fma(m, lds_f64(tb + k8), -1.0);
+    const double r2 = r * r;
+    double P = fma(-1.0 / 6.0, r, 1.0 / 5.0);
+    P = fma(P, r, -0.25);
+    P = fma(P, r, 1.0 / 3.0);
+    P = fma(P, r, -0.5);
+    const double u = r2 * P;  // ln(1 + r) = r + u
+    const double K_hi = 1.4426950408889634, K_lo = 2.0355273740931033e-17;  // 1 / ln 2
+    const double s_hi = r * K_hi;
+    double s_lo = fma(r, K_hi, -s_hi);
+    s_lo = fma(r, K_lo, s_lo);
+    s_lo = fma(u, K_hi, s_lo);
+    const double L = lds_f64(tb + 1024 + k8) + (s_hi + (s_lo + lds_f64(tb + 2048 + k8)));
+    const long long q = ((long long)e << 51) + __double2ll_rn(L * 0x1p51);
+    return (unsigned long long)q + (x < 0.0 ? 0x8000000000000000ull : 0ull);
+}
 __device__ __forceinline__ unsigned long long mul_code(double x, const Log2Tab &tb) {
     long long b = __double_as_longlong(x) & 0x7fffffffffffffffll;
     int e = (int)(b >> 52);
@@ -331,14 +364,14 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) rbi_fwd_smem_log(const
     const uint64_t m = (uint64_t)P.m;
     // 32-bit shared-window addresses, computed once (the generic-pointer
     // atomics re-derived the window base for every element)
-    const uint32_t a_lo = smem_u32(lo), a_hi = smem_u32(hi), a_zc = smem_u32(zc);
+    const uint32_t a_lo = smem_u32(lo), a_hi = smem_u32(hi), a_zc = smem_u32(zc), a_tb = smem_u32(&tb);
     auto visit = [&](int64_t b, double x) {
         if ((uint64_t)b >= m) return;  // out-of-range bins (negative ones wrap): skipped (R4)
         const uint32_t o = (uint32_t)b * 4u;
         if (x == 0.0) {
             asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(a_zc + o) : "memory");
         } else {
-            const unsigned long long q = mul_code(x, tb);
+            const unsigned long long q = mul_code_s(x, a_tb);
             const unsigned ql = (unsigned)q;
             unsigned old;
             asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a_lo + o), "r"(ql) : "memory");
@@ -520,22 +553,6 @@ __global__ void rbi_mul_prep(const T *__restrict__ hs_bar, const double *__restr
     }
 }
 
-// q / a without the IEEE division's subroutine: reciprocal estimate, two
-// Newton steps, the product and one residual correction (within 1 ulp of the
-// correctly rounded quotient); a outside [2^-1000, 2^1000] (where the
-// estimate's flush-to-zero or the reciprocal's range matter) takes the IEEE
-// division
-__device__ __forceinline__ double div_fast(double q, double a) {
-    const double aa = fabs(a);
-    if (!(aa > 0x1p-1000 && aa < 0x1p1000)) return q / a;
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
-    r = fma(r, fma(-a, r, 1.0), r);
-    r = fma(r, fma(-a, r, 1.0), r);
-    const double y = q * r;
-    return fma(r, fma(-a, y, q), y);
-}
-
 // ADD (gather) and MUL (three cases) return map; lane-contiguous 4-element
 // groups, two slabs per iteration for 8 independent gathers in flight per lane
 template <class T, class I, int OP>
@@ -554,7 +571,7 @@ __device__ __forceinline__ void rbi_bwd_map_body(const I *__restrict__ inds, con
         const int64_t z = (int64_t)__double_as_longlong(k.y);
         if (z == 0) {
             touch = true;
-            return div_fast(k.x, a);  // hs_bar_b * y_b / a_i
+            return k.x / a;  // hs_bar_b * y_b / a_i
         }
         touch = (z == 1 && a == 0.0);  // P:1048-1053 per bin
         return touch ? k.x : 0.0;
