@@ -656,7 +656,9 @@ def run_extra(args):
                 a = (1.0 + (synth.uniform(n, 7, device=dev) - 0.5) * 2.0 ** -6).to(td)
                 yb = synth.uniform(n, 8, dtype=td, device=dev)
             out = torch.empty_like(yb)
-            nb = (2 if args.op == "add" else 4) * width * es
+            # method bytes: ADD 2 arrays; MUL/LINREC/MAT2 4 (as read by the forward
+            # re-execution and the return sweep); MIN/MAX 3 (as the round-1 lines count them)
+            nb = (2 if args.op == "add" else (3 if args.op in ("min", "max") else 4)) * width * es
             cases.append((f"scan {args.op.upper()} {args.dtype} n={n}", n, nb * n,
                           lambda: vjp.scan(args.op, yb, a, out=out)))
         elif args.kind == "reduce":

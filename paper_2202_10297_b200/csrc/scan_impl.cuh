@@ -10,6 +10,7 @@
 
 #include "scan_blocklb.cuh"
 #include "scan_add1p.cuh"
+#include "scan_ext1p.cuh"
 
 namespace vjph {
 
@@ -77,7 +78,7 @@ struct ScanImpl {
         size_t counters, flags1, flags2, memset_bytes, p1agg, p1inc, p2agg, p2inc, partial;
         int64_t ntiles_c;
         size_t tileF, tileP, chunkRec, counter_c, roundRec, arrive, lbFlags, lbAgg, lbInc, lbTileF, lbTileP, lbPark,
-            p1Ctr, p1Agg, p1Inc, p1Grp, p1End, total;
+            p1Ctr, p1Agg, p1Inc, p1Grp, p1End, pxCtr, pxAgg, pxInc, pxGrp, pxEnd, total;
         int64_t p1Tiles;
     };
     static Layout layout(int64_t n) {
@@ -118,6 +119,15 @@ struct ScanImpl {
         L.p1Inc = off; off += align256((size_t)L.p1Tiles * 16);
         L.p1Grp = off; off += align256((size_t)p1g * 16);
         L.p1End = off;
+        // one-pass MIN/MAX return (scan_ext1p.cuh): records per 256-row tile
+        {
+            const int64_t xg = (L.ntiles + 31) / 32;
+            L.pxCtr = off; off += align256(256 + (size_t)xg * 4);
+            L.pxAgg = off; off += align256((size_t)L.ntiles * 16);
+            L.pxInc = off; off += align256((size_t)L.ntiles * 16);
+            L.pxGrp = off; off += align256((size_t)xg * 16);
+            L.pxEnd = off;
+        }
         L.total = off;
         return L;
     }
@@ -848,8 +858,55 @@ struct ScanImpl {
                   : launch_apply_rs<false, false>(c, p, ma, my, mab, mys);
     }
 
+    // ---------------- MIN/MAX: K_F + one return pass with look-back (scan_ext1p.cuh) ----------------
+    static bool use_ext1p(const ScanCall &c) {
+        if constexpr (!Op::kRevNeedsRs) {
+            return false;
+        } else {
+            if (c.world != 1 || c.ys || c.cyc) return false;
+            return !(c.flags & (VJP_SCAN_LOOKBACK | VJP_SCAN_CHUNKED | VJP_ACCUMULATE));
+        }
+    }
+    static vjp_status finish_ext1p(const ScanCall &c) {
+        if constexpr (!Op::kRevNeedsRs) {
+            return VJP_EUNSUPPORTED;
+        } else {
+            Layout L = layout(c.n);
+            vjpk::ChunkParams pf = cparams(c, L, nchunks_fwd(L));
+            vjpk::scan_tile_prefix<Op, NTC><<<(unsigned)pf.nchunks, NTC, 0, c.stream>>>(pf);
+            unsigned char *ws = static_cast<unsigned char *>(c.ws);
+            if (cudaMemsetAsync(ws + L.pxCtr, 0, L.pxEnd - L.pxCtr, c.stream) != cudaSuccess) return VJP_ECUDA;
+            vjpk::Ext1pParams X{};
+            X.r.n = c.n;
+            X.r.ntiles = L.ntiles;
+            X.r.ys_bar = c.ys_bar;
+            X.r.as_bar = c.as_bar;
+            X.r.ticket = reinterpret_cast<uint32_t *>(ws + L.pxCtr);
+            X.r.gcount = reinterpret_cast<uint32_t *>(ws + L.pxCtr + 256);
+            X.r.agg = reinterpret_cast<double2 *>(ws + L.pxAgg);
+            X.r.inc = reinterpret_cast<double2 *>(ws + L.pxInc);
+            X.r.grp = reinterpret_cast<double2 *>(ws + L.pxGrp);
+            X.as = c.as;
+            X.tileP = pf.tileP;
+            X.global_first = c.global_offset == 0 ? 1 : 0;
+            const int64_t rows = c.n * (int64_t)sizeof(T) / vjpk::kRowBytes;
+            CUtensorMap ma, my, mo;
+            const bool f64 = sizeof(T) == 8;
+            if (!make_row_tmap(&ma, c.as, rows, f64, 256) || !make_row_tmap(&my, c.ys_bar, rows, f64, 256) ||
+                !make_row_tmap(&mo, c.as_bar, rows, f64, 256))
+                return VJP_ECUDA;
+            constexpr size_t sm = 1024 + (size_t)2 * vjpk::k1pData * 128;
+            auto k = vjpk::scan_ext_1p<Op, T>;
+            set_smem(k, sm);
+            k<<<(unsigned)L.ntiles, vjpk::k1pData + 32, sm, c.stream>>>(ma, my, mo, X);
+            count_launch(2);
+            return cudaGetLastError() == cudaSuccess ? VJP_OK : VJP_ECUDA;
+        }
+    }
+
     static vjp_status partial(const ScanCall &c) {
         if (use_1p(c)) return VJP_OK;             // one pass, in finish
+        if (use_ext1p(c)) return partial_rs(c);   // K_F: forward tile aggregates of `as`
         if (use_lb(c)) return phase_lb(c, true);  // the `as`-only forward pre-pass K_F (nothing for scan(+))
         if constexpr (Op::kRevNeedsRs) {
             if (use_rs_chunked(c)) return partial_rs(c);
@@ -877,6 +934,7 @@ struct ScanImpl {
 
     static vjp_status finish(const ScanCall &c) {
         if (use_1p(c)) return launch_1p(c);
+        if (use_ext1p(c)) return finish_ext1p(c);
         if (use_lb(c)) return phase_lb(c, false);
         if constexpr (Op::kRevNeedsRs) {
             if (use_rs_chunked(c)) return finish_rs(c);
