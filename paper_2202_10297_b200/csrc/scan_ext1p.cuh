@@ -155,7 +155,7 @@ __device__ __forceinline__ ExtMap ext_compose(const ExtMap &o, const ExtMap &i) 
 }
 
 template <class Op, class T>
-__global__ void __launch_bounds__(k1pData + 32, 2) scan_ext_1p(const __grid_constant__ CUtensorMap tm_as,
+__global__ void __launch_bounds__(k1pData + 32, 3) scan_ext_1p(const __grid_constant__ CUtensorMap tm_as,
                                                              const __grid_constant__ CUtensorMap tm_yb,
                                                              const __grid_constant__ CUtensorMap tm_out,
                                                              const Ext1pParams X) {
