@@ -50,5 +50,29 @@ for n, k, d in ((1, 1, 1), (129, 65, 17), (5000, 100, 64), (3000, 20, 70)):  # c
     for dt in (torch.float64, torch.float32):
         P, C = synth.kmeans_inputs(n, k, d, dtype=dt, device=dev)
         vjp.kmeans(P, C, 1.0)
+# round 2: one-pass scan(+) and MIN/MAX (f32 / f64, ragged), chunked ADD,
+# vectorised reduce_by_index, the deterministic ADD primal (bin sort), the
+# block-cyclic sweep on one rank
+for dt in (torch.float64, torch.float32):
+    for n in (1, 5000, 300_001):
+        yb = synth.uniform(n, 2, dtype=dt, device=dev)
+        vjp.scan('add', yb)
+        vjp.scan('add', yb, chunked=True)
+        a = synth.min_inputs(n, dtype=dt, device=dev)
+        vjp.scan('min', yb, a)
+        vjp.scan('max', yb, a)
+for op in ('add', 'mul', 'min', 'max'):
+    for width in (3, 33):
+        inds, a, hb = synth.rbi_wide_inputs(2001, 77, width, op, device=dev)
+        vjp.reduce_by_index(op, inds, a, hb, want_hs=True, width=width)
+inds, a, hb = synth.rbi_inputs(100_003, 500, 'add', device=dev)
+vjp.reduce_by_index('add', inds, a, hb, want_hs=True)
+from paper_2202_10297_b200 import dist as vdist
+for op in ('add', 'linrec'):
+    n = 300_001
+    w = vjp.WIDTH[vjp.OPS[op]]
+    a = 0.5 + synth.uniform(n * w, 1, device=dev) if op != 'add' else None
+    yb = synth.uniform(n * w, 2, device=dev)
+    vdist.scan_cyclic(op, yb, a, global_n=n, sb_elems=vjp.lib().vjp_scan_cyclic_tile_elems(vjp.OPS[op], 2) * 8)
 torch.cuda.synchronize()
 print('sanitize cases done')
