@@ -54,6 +54,24 @@ __device__ __forceinline__ double2 ld_rec16(const double2 *p) {
     return r;
 }
 
+// 16-byte chunk <-> 2 f64 / 4 f32 elements, by value (no address of a
+// register array: that would put the row in local memory)
+__device__ __forceinline__ void unpack16(const double2 &w, double *v) { v[0] = w.x; v[1] = w.y; }
+__device__ __forceinline__ void unpack16(const double2 &w, float *v) {
+    const unsigned long long a = (unsigned long long)__double_as_longlong(w.x);
+    const unsigned long long b = (unsigned long long)__double_as_longlong(w.y);
+    v[0] = __uint_as_float((unsigned)a);
+    v[1] = __uint_as_float((unsigned)(a >> 32));
+    v[2] = __uint_as_float((unsigned)b);
+    v[3] = __uint_as_float((unsigned)(b >> 32));
+}
+__device__ __forceinline__ double2 pack16(const double *v) { return make_double2(v[0], v[1]); }
+__device__ __forceinline__ double2 pack16(const float *v) {
+    const unsigned long long a = (unsigned long long)__float_as_uint(v[0]) | ((unsigned long long)__float_as_uint(v[1]) << 32);
+    const unsigned long long b = (unsigned long long)__float_as_uint(v[2]) | ((unsigned long long)__float_as_uint(v[3]) << 32);
+    return make_double2(__longlong_as_double((long long)a), __longlong_as_double((long long)b));
+}
+
 // exclusive sum of everything right of ticket k (one warp; result in every
 // lane).  Level 1 covers the D (97..128) tickets just below k, down to a
 // group boundary 32 G0, reading their records DIRECTLY (4 per lane, all
@@ -139,8 +157,11 @@ __device__ __forceinline__ uint32_t atom_add_release_gpu(uint32_t *p, uint32_t v
     asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
     return old;
 }
+// named barrier WITHOUT .aligned (bar.sync is barrier.sync.aligned, which
+// requires the whole warp converged at the instruction — the look-back warp
+// arrives from per-lane polling loops; compute-sanitizer synccheck flags it)
 __device__ __forceinline__ void bar_named(int id, int count) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+    asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
 // 8 data warps + 1 look-back warp that computes the exclusive sum WHILE the
@@ -151,7 +172,7 @@ __device__ __forceinline__ void bar_named(int id, int count) {
 // RPT t .. RPT t + RPT - 1 and reads / writes them conflict-free (swz).
 constexpr int k1pData = 256;
 template <class T, int RPT>
-__global__ void __launch_bounds__(k1pData + 32) scan_add_1p(const __grid_constant__ CUtensorMap tm_in,
+__global__ void __launch_bounds__(k1pData + 32, 2) scan_add_1p(const __grid_constant__ CUtensorMap tm_in,
                                                              const __grid_constant__ CUtensorMap tm_out,
                                                              const Add1pParams P) {
     constexpr int E = 128 / (int)sizeof(T);  // elements per row
@@ -210,21 +231,22 @@ __global__ void __launch_bounds__(k1pData + 32) scan_add_1p(const __grid_constan
         bar_named(2, k1pData);
     }
     mbar_wait(&s_bar, 0);
-    // pass 1: the thread's sum over its RPT rows (chunk order rotated by lane)
+    // pass 1: the thread's sum over its RPT rows (8 independent chunk sums per
+    // row, added as a tree: short dependent chains)
     double rs = 0.0;
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
         const int r = RPT * t + i;
+        double cs[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-            const double2 w = *reinterpret_cast<const double2 *>(s_tile + swz(r, c));
-            if (sizeof(T) == 8) {
-                rs += w.x + w.y;
-            } else {
-                const float4 f = *reinterpret_cast<const float4 *>(&w);
-                rs += ((double)f.x + (double)f.y) + ((double)f.z + (double)f.w);
-            }
+            T v[EPC];
+            unpack16(*reinterpret_cast<const double2 *>(s_tile + swz(r, c)), v);
+            cs[c] = 0.0;
+#pragma unroll
+            for (int q = 0; q < EPC; ++q) cs[c] += (double)v[q];
         }
+        rs += ((cs[0] + cs[1]) + (cs[2] + cs[3])) + ((cs[4] + cs[5]) + (cs[6] + cs[7]));
     }
     double sw = rs;  // inclusive suffix over the warp (lanes to the right = higher elements)
 #pragma unroll
@@ -266,26 +288,35 @@ __global__ void __launch_bounds__(k1pData + 32) scan_add_1p(const __grid_constan
     }
     bar_named(1, k1pData + 32);
     double carry = s_excl + right_warps + (sw - rs);
-    // pass 2: rows right to left; a row is read whole, its suffix sums written back in place
+    // pass 2: rows right to left; per row the 8 chunk sums first, then the
+    // suffix over the chunks, then inside each chunk (dependent chain 8 + EPC
+    // instead of E); results written back in place
 #pragma unroll
     for (int i = RPT - 1; i >= 0; --i) {
         const int r = RPT * t + i;
         T v[E];
+        double cs[8];
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
-            const double2 w = *reinterpret_cast<const double2 *>(s_tile + swz(r, c));
-            const T *wt = reinterpret_cast<const T *>(&w);
+            unpack16(*reinterpret_cast<const double2 *>(s_tile + swz(r, c)), v + c * EPC);
+            cs[c] = 0.0;
 #pragma unroll
-            for (int q = 0; q < EPC; ++q) v[c * EPC + q] = wt[q];
+            for (int q = 0; q < EPC; ++q) cs[c] += (double)v[c * EPC + q];
         }
+        double suf = carry;  // entering chunk c from the right
 #pragma unroll
-        for (int q = E - 1; q >= 0; --q) {
-            carry += (double)v[q];
-            v[q] = (T)carry;
+        for (int c = 7; c >= 0; --c) {
+            double run = suf;
+#pragma unroll
+            for (int q = EPC - 1; q >= 0; --q) {
+                run += (double)v[c * EPC + q];
+                v[c * EPC + q] = (T)run;
+            }
+            suf += cs[c];
         }
+        carry = suf;
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
-            *reinterpret_cast<double2 *>(s_tile + swz(r, c)) = *reinterpret_cast<const double2 *>(&v[c * EPC]);
+        for (int c = 0; c < 8; ++c) *reinterpret_cast<double2 *>(s_tile + swz(r, c)) = pack16(v + c * EPC);
     }
     if (full) {
         fence_proxy_async_smem();

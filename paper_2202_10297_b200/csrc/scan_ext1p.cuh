@@ -127,24 +127,6 @@ __device__ __forceinline__ double ext1p_lookback(const Add1pParams &P, int64_t k
     return sum;
 }
 
-// 16-byte chunk <-> 2 f64 / 4 f32 elements, by value (no address of a
-// register array: that would put the row in local memory)
-__device__ __forceinline__ void unpack16(const double2 &w, double *v) { v[0] = w.x; v[1] = w.y; }
-__device__ __forceinline__ void unpack16(const double2 &w, float *v) {
-    const unsigned long long a = (unsigned long long)__double_as_longlong(w.x);
-    const unsigned long long b = (unsigned long long)__double_as_longlong(w.y);
-    v[0] = __uint_as_float((unsigned)a);
-    v[1] = __uint_as_float((unsigned)(a >> 32));
-    v[2] = __uint_as_float((unsigned)b);
-    v[3] = __uint_as_float((unsigned)(b >> 32));
-}
-__device__ __forceinline__ double2 pack16(const double *v) { return make_double2(v[0], v[1]); }
-__device__ __forceinline__ double2 pack16(const float *v) {
-    const unsigned long long a = (unsigned long long)__float_as_uint(v[0]) | ((unsigned long long)__float_as_uint(v[1]) << 32);
-    const unsigned long long b = (unsigned long long)__float_as_uint(v[2]) | ((unsigned long long)__float_as_uint(v[3]) << 32);
-    return make_double2(__longlong_as_double((long long)a), __longlong_as_double((long long)b));
-}
-
 // (D, C) maps: o after i (i applied first)
 struct ExtMap {
     double D;
