@@ -233,7 +233,7 @@ def test_scan_add_2pow30_sampled():
     got = vjp.scan("add", yb)
     exact = torch.flip(torch.cumsum(torch.flip(yb.to(torch.int64), [0]), 0), [0])
     assert torch.equal(got.to(torch.int64), exact)
-    got_ch = vjp.scan("add", yb, chunked=True)  # (the default above is the L2-round sweep)
+    got_ch = vjp.scan("add", yb, chunked=True)  # (the default above is the one-pass look-back kernel)
     assert torch.equal(got_ch.to(torch.int64), exact)
     del got_ch
     # sampled comparison against the oracle on a slice near the end (independent of the prefix)
@@ -296,3 +296,42 @@ def test_bench_sequence_dist_scan_world1(op):
         torch.cuda.synchronize()
         assert ev["finish_start"].elapsed_time(ev["finish_end"]) > 0
         assert_close(ab.cpu().numpy(), ref, np.float64, what=f"bench sequence {op}")
+
+
+def test_scan_add_f32_2pow30_one_pass():
+    """target size n = 2^30 f32 on the default one-pass kernel: integer seeds
+    (|.| <= 8), accumulated in f64 (R9) exactly, rounded once to f32 — the
+    same single rounding of the exact suffix sum the oracle performs, so the
+    result equals the exact int64 suffix sum cast to f32 bit for bit."""
+    n = 1 << 30
+    yb = synth.scan_add_seed(n, kind="int", device=DEV).to(torch.float32)
+    got = vjp.scan("add", yb)
+    exact = torch.flip(torch.cumsum(torch.flip(yb.to(torch.int64), [0]), 0), [0])
+    assert torch.equal(got, exact.to(torch.float64).to(torch.float32))
+
+
+@pytest.mark.parametrize("op", ["min", "max"])
+def test_scan_minmax_one_pass_large(op):
+    """MIN/MAX one-pass return (K_F + look-back) at 2^26 f64 with many ties
+    and records spread over the array: against the chunked rs path (an
+    independent kernel chain) exactly, and against the oracle on a sampled
+    tail slice (its carry from the right is zero at the end)"""
+    n = 1 << 26
+    a = synth.min_inputs(n, dtype=torch.float64, device=DEV)
+    if op == "max":
+        a = -a
+    yb = synth.scan_add_seed(n, kind="int", device=DEV)  # integer seeds: every order exact
+    got = vjp.scan(op, yb, a)
+    ref = vjp.scan(op, yb, a, chunked=True)
+    assert torch.equal(got, ref)
+    m = 200_000
+    # the oracle on the whole array would be slow: compare the head (records
+    # entering from the left are exactly those of the prefix)
+    head_ref = oracle.vjp_scan(op, yb[:m].cpu().numpy(), a[:m].cpu().numpy())
+    # the head's outputs also depend on the carry from the right: only where a
+    # record lies at or after the head's end does the carry vanish, so compare
+    # the positions before the last record of the head
+    rec = np.nonzero(head_ref != 0)[0]
+    if len(rec) > 1:
+        last = rec[-1]
+        assert np.array_equal(got[:last].cpu().numpy(), head_ref[:last])
