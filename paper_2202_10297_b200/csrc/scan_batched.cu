@@ -45,7 +45,7 @@ struct BatParams {
     const void *as;
     const void *ys_bar;
     void *as_bar;
-    double *rec;     // [C][w][W + MD]
+    double *rec;     // [w][C][W + MD] (a column's chunk records contiguous for scan_bat_carries)
     double *tileP;   // [C * TPC][w][W] exclusive forward prefix of each tile inside its chunk
     double *carry;   // [C][w][2W]  {forward prefix entering the chunk, reverse carry entering it}
     int32_t acc;
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kBatThreads) scan_bat_reduce(const BatParams p
 #pragma unroll
     for (int q = 0; q < W; ++q) rec[q] = F.x[q];
     map_to<Op>(Mc, rec + W);
-    double *dst = p.rec + (c * p.w + j) * (W + MD);
+    double *dst = p.rec + (j * p.C + c) * (W + MD);  // column-major: a column's chunk records contiguous
 #pragma unroll
     for (int q = 0; q < W + MD; ++q) dst[q] = rec[q];
 }
@@ -153,26 +153,30 @@ __global__ void __launch_bounds__(kBatThreads) scan_bat_maps_rs(const BatParams 
     }
     double rec[MD];
     map_to<Op>(Mc, rec);
-    double *dst = p.rec + (c * p.w + j) * (W + MD) + W;
+    double *dst = p.rec + (j * p.C + c) * (W + MD) + W;
 #pragma unroll
     for (int q = 0; q < MD; ++q) dst[q] = rec[q];
 }
 
-// one CTA (256 threads) per column: exclusive scans over the C chunk records
+// one CTA of 1024 threads per column: exclusive scans over the C chunk
+// records (~SMs x 2048 / w of them: 1024 threads keep each thread's serial
+// walk short — 256 threads left it latency bound: 96 us for LINREC w = 32)
+constexpr int kBatCarryThreads = 1024;
 template <class Op>
-__global__ void __launch_bounds__(256) scan_bat_carries(const BatParams p) {
+__global__ void __launch_bounds__(kBatCarryThreads) scan_bat_carries(const BatParams p) {
     using V = typename Op::Val;
     using M = typename Op::Map;
-    constexpr int W = Op::W, MD = Op::kMapD, R = W + MD;
-    __shared__ V vs[9];
-    __shared__ M ms[9];
+    constexpr int W = Op::W, MD = Op::kMapD, R = W + MD, NW = kBatCarryThreads / 32;
+    __shared__ V vs[NW + 1];
+    __shared__ M ms[NW + 1];
     const int64_t j = blockIdx.x;
     const int t = threadIdx.x;
-    const int64_t per = (p.C + 255) / 256, c0 = t * per, c1 = c0 + per < p.C ? c0 + per : p.C;
+    const int64_t per = (p.C + kBatCarryThreads - 1) / kBatCarryThreads, c0 = t * per,
+                  c1 = c0 + per < p.C ? c0 + per : p.C;
     V f = Op::fwd_id();
     M m = Op::map_id();
     for (int64_t c = c0; c < c1; ++c) {
-        const double *r = p.rec + (c * p.w + j) * R;
+        const double *r = p.rec + (j * p.C + c) * R;
         V v;
 #pragma unroll
         for (int q = 0; q < W; ++q) v.x[q] = r[q];
@@ -181,8 +185,8 @@ __global__ void __launch_bounds__(256) scan_bat_carries(const BatParams p) {
     }
     V ftot;
     M mtot;
-    V fpre = block_excl_fwd<Op, 8>(f, vs, ftot);   // chunks before this thread's range
-    M mpost = block_excl_rev<Op, 8>(m, ms, mtot);  // chunks after it
+    V fpre = block_excl_fwd<Op, NW>(f, vs, ftot);   // chunks before this thread's range
+    M mpost = block_excl_rev<Op, NW>(m, ms, mtot);  // chunks after it
     V x;
 #pragma unroll
     for (int q = 0; q < W; ++q) x.x[q] = 0.0;
@@ -192,7 +196,7 @@ __global__ void __launch_bounds__(256) scan_bat_carries(const BatParams p) {
         double *cr = p.carry + (c * p.w + j) * 2 * W;
 #pragma unroll
         for (int q = 0; q < W; ++q) cr[q] = fpre.x[q];
-        const double *r = p.rec + (c * p.w + j) * R;
+        const double *r = p.rec + (j * p.C + c) * R;
         V v;
 #pragma unroll
         for (int q = 0; q < W; ++q) v.x[q] = r[q];
@@ -202,7 +206,7 @@ __global__ void __launch_bounds__(256) scan_bat_carries(const BatParams p) {
         double *cr = p.carry + (c * p.w + j) * 2 * W;
 #pragma unroll
         for (int q = 0; q < W; ++q) cr[W + q] = x.x[q];
-        x = Op::apply(map_from<Op>(p.rec + (c * p.w + j) * R + W), x);
+        x = Op::apply(map_from<Op>(p.rec + (j * p.C + c) * R + W), x);
     }
 }
 
@@ -331,13 +335,13 @@ vjp_status bat_run(int64_t n, int64_t w, const void *as, const void *yb, void *a
         // MIN/MAX: forward records -> forward prefixes -> maps with the true rs
         // -> carries again (forward prefixes recomputed identically, reverse now valid)
         vjpk::scan_bat_reduce<Op, T, true, false><<<grid, vjpk::kBatThreads, 0, s>>>(p);
-        vjpk::scan_bat_carries<Op><<<(unsigned)w, 256, 0, s>>>(p);
+        vjpk::scan_bat_carries<Op><<<(unsigned)w, vjpk::kBatCarryThreads, 0, s>>>(p);
         vjpk::scan_bat_maps_rs<Op, T><<<grid, vjpk::kBatThreads, 0, s>>>(p);
         count_launch(2);
     } else {
         vjpk::scan_bat_reduce<Op, T, FWD><<<grid, vjpk::kBatThreads, 0, s>>>(p);
     }
-    vjpk::scan_bat_carries<Op><<<(unsigned)w, 256, 0, s>>>(p);
+    vjpk::scan_bat_carries<Op><<<(unsigned)w, vjpk::kBatCarryThreads, 0, s>>>(p);
     if (p.acc)
         vjpk::scan_bat_apply<Op, T, FWD, true><<<grid, vjpk::kBatThreads, 0, s>>>(p);
     else
