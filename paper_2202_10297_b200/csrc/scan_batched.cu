@@ -47,7 +47,7 @@ struct BatParams {
     void *as_bar;
     double *rec;     // [w][C][W + MD] (a column's chunk records contiguous for scan_bat_carries)
     double *tileP;   // [C * TPC][w][W] exclusive forward prefix of each tile inside its chunk
-    double *carry;   // [C][w][2W]  {forward prefix entering the chunk, reverse carry entering it}
+    double *carry;   // [w][C][2W]  {forward prefix entering the chunk, reverse carry entering it}
     int32_t acc;
 };
 
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kBatThreads) scan_bat_maps_rs(const BatParams 
     if (!bat_coord(p, c, j)) return;
     const T *as = static_cast<const T *>(p.as);
     const T *yb = static_cast<const T *>(p.ys_bar);
-    const double *cr = p.carry + (c * p.w + j) * 2 * W;
+    const double *cr = p.carry + (j * p.C + c) * 2 * W;
     V rs;
 #pragma unroll
     for (int q = 0; q < W; ++q) rs.x[q] = cr[q];
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(kBatCarryThreads) scan_bat_carries(const BatPa
     x = Op::apply(mpost, x);  // reverse carry entering the thread's last chunk from the right
     // forward prefixes ascending, reverse carries descending
     for (int64_t c = c0; c < c1; ++c) {
-        double *cr = p.carry + (c * p.w + j) * 2 * W;
+        double *cr = p.carry + (j * p.C + c) * 2 * W;
 #pragma unroll
         for (int q = 0; q < W; ++q) cr[q] = fpre.x[q];
         const double *r = p.rec + (j * p.C + c) * R;
@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(kBatCarryThreads) scan_bat_carries(const BatPa
         fpre = Op::fwd(fpre, v);
     }
     for (int64_t c = c1 - 1; c >= c0; --c) {
-        double *cr = p.carry + (c * p.w + j) * 2 * W;
+        double *cr = p.carry + (j * p.C + c) * 2 * W;
 #pragma unroll
         for (int q = 0; q < W; ++q) cr[W + q] = x.x[q];
         x = Op::apply(map_from<Op>(p.rec + (j * p.C + c) * R + W), x);
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kBatThreads) scan_bat_apply(const BatParams p)
     const T *as = static_cast<const T *>(p.as);
     const T *yb = static_cast<const T *>(p.ys_bar);
     T *ab = static_cast<T *>(p.as_bar);
-    const double *cr = p.carry + (c * p.w + j) * 2 * W;
+    const double *cr = p.carry + (j * p.C + c) * 2 * W;
     V F0, X;
 #pragma unroll
     for (int q = 0; q < W; ++q) {
