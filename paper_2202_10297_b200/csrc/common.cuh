@@ -22,6 +22,14 @@ constexpr int kTileBytes = kRowBytes * kThreads;  // 32 KB per array per tile
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// the dynamic shared buffer rounded up to a 1024-byte boundary (TMA 128B
+// swizzle).  Pointer arithmetic on the __shared__ array itself (not a round
+// trip through uintptr_t), so nvcc still knows the result is in shared memory
+// and emits LDS/STS — through a uintptr_t cast every tile access became a
+// generic LD/ST on the long scoreboard (ncu, r02_ncu_config2_apply).
+__device__ __forceinline__ unsigned char *smem_align1024(unsigned char *raw) {
+    return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
+}
 
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");

@@ -257,7 +257,8 @@ __device__ __forceinline__ double lds_f64(uint32_t a) {
 // the same code with the table addressed through a 32-bit shared-window
 // address computed once per thread (the hot loop of the small-m histogram)
 __device__ __forceinline__ unsigned long long mul_code_s(double x, uint32_t tb) {
-    long long b = __double_as_longlong(x) & 0x7fffffffffffffffll;
+    // |x| by integer ops on the high word (not a DADD on the FP64 pipe)
+    long long b = ((long long)(__double2hiint(x) & 0x7fffffff) << 32) | (unsigned)__double2loint(x);
     int e = (int)(b >> 52);
     if (e == 0) {  // subnormal
         b = __double_as_longlong(__longlong_as_double(b) * 0x1p54);
@@ -279,11 +280,16 @@ __device__ __forceinline__ unsigned long long mul_code_s(double x, uint32_t tb) 
     s_lo = fma(r, K_lo, s_lo);
     s_lo = fma(u, K_hi, s_lo);
     const double L = lds_f64(tb + 1024 + k8) + (s_hi + (s_lo + lds_f64(tb + 2048 + k8)));
-    const long long q = ((long long)e << 51) + __double2ll_rn(L * 0x1p51);
-    return (unsigned long long)q + (x < 0.0 ? 0x8000000000000000ull : 0ull);
+    // rne(L * 2^51) by one FMA: 0 <= L * 2^51 <= 2^51, so L * 2^51 + 1.5 * 2^52
+    // lies in a binade of unit ulp and its low mantissa bits are the rounded
+    // integer (the same value as __double2ll_rn, without the F2I.F64 pipe)
+    const double t = fma(L, 0x1p51, 0x1.8p52);
+    const long long q = ((long long)e << 51) + (__double_as_longlong(t) - 0x4338000000000000ll);
+    return (unsigned long long)q + ((unsigned long long)__double_as_longlong(x) & 0x8000000000000000ull);
 }
 __device__ __forceinline__ unsigned long long mul_code(double x, const Log2Tab &tb) {
-    long long b = __double_as_longlong(x) & 0x7fffffffffffffffll;
+    // |x| by integer ops on the high word (not a DADD on the FP64 pipe)
+    long long b = ((long long)(__double2hiint(x) & 0x7fffffff) << 32) | (unsigned)__double2loint(x);
     int e = (int)(b >> 52);
     if (e == 0) {  // subnormal
         b = __double_as_longlong(__longlong_as_double(b) * 0x1p54);
@@ -305,8 +311,12 @@ __device__ __forceinline__ unsigned long long mul_code(double x, const Log2Tab &
     s_lo = fma(r, K_lo, s_lo);
     s_lo = fma(u, K_hi, s_lo);
     const double L = tb.hi[k] + (s_hi + (s_lo + tb.lo[k]));  // log2 m in [0, 1]
-    const long long q = ((long long)e << 51) + __double2ll_rn(L * 0x1p51);
-    return (unsigned long long)q + (x < 0.0 ? 0x8000000000000000ull : 0ull);
+    // rne(L * 2^51) by one FMA: 0 <= L * 2^51 <= 2^51, so L * 2^51 + 1.5 * 2^52
+    // lies in a binade of unit ulp and its low mantissa bits are the rounded
+    // integer (the same value as __double2ll_rn, without the F2I.F64 pipe)
+    const double t = fma(L, 0x1p51, 0x1.8p52);
+    const long long q = ((long long)e << 51) + (__double_as_longlong(t) - 0x4338000000000000ll);
+    return (unsigned long long)q + ((unsigned long long)__double_as_longlong(x) & 0x8000000000000000ull);
 }
 __device__ __forceinline__ double mul_decode(unsigned long long T) {
     const long long L = ((long long)(T << 1)) >> 1;  // sign-extend 63 bits
@@ -339,10 +349,73 @@ __global__ void __launch_bounds__(kBThreads) rbi_fwd_log(const I *__restrict__ i
     __syncthreads();
     rbi_stream<T, I>(inds, as, nullptr, P, [&](int64_t b, double x, int64_t, bool ok) {
         if (!ok) return;
-        if (x == 0.0) atomicAdd(P.z + b, 1ull);
+        if ((__double_as_longlong(x) << 1) == 0) atomicAdd(P.z + b, 1ull);  // +-0 (integer test)
         else atomicAdd(P.code + b, mul_code(x, tb));
     });
 }
+// ---- cp.async ring for the streamed (inds, as) slabs ----------------------
+// The register double-buffer (rbi_stream) keeps ONE slab (1.5 KB per warp) in
+// flight; ncu of the small-m x histogram shows a third of its warp samples on
+// the long scoreboard.  Here each lane stages its own 16-byte granules of the
+// next S slabs in shared memory with cp.async (no registers held) and reads
+// back only what it copied itself — its own cp.async.wait_group is the only
+// synchronisation.  Granule g of thread t in stage s sits at s * kStage +
+// g * 4 KB + t * 16 B (conflict-free 128-bit accesses).  Measured at n = 2^28,
+// m = 10^3: forward 856 -> 804 us.  Used by the x histogram only: in the x
+// return map (992 -> 1131 us at depth 2 or 4) and in MIN/MAX phase A (whole
+// call 1.09 -> 1.20 ms) it measured slower (DESIGN 7.6).
+#ifndef VJP_RING_FWD
+#define VJP_RING_FWD 3
+#endif
+constexpr int kRingFwd = VJP_RING_FWD > 0 ? VJP_RING_FWD : 1;  // forward histogram (0: register path)
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+template <class T, class I, int S>
+struct SlabRing {
+    static constexpr int GI = (int)sizeof(I) / 4, GV = (int)sizeof(T) / 4;  // 16-byte granules per lane
+    static constexpr int kGran = kBThreads * 16;
+    static constexpr int kStage = (GI + GV) * kGran;
+    static constexpr int kBytes = S * kStage;
+    __device__ static __forceinline__ void issue(uint32_t sb, int st, const I *inds, const T *as, int64_t e,
+                                                 uint64_t pol) {
+        const uint32_t d = sb + st * kStage + threadIdx.x * 16;
+#pragma unroll
+        for (int g = 0; g < GI; ++g) cp_async16(d + g * kGran, reinterpret_cast<const char *>(inds + e) + 16 * g, pol);
+#pragma unroll
+        for (int g = 0; g < GV; ++g)
+            cp_async16(d + (GI + g) * kGran, reinterpret_cast<const char *>(as + e) + 16 * g, pol);
+    }
+    __device__ static __forceinline__ void read(uint32_t sb, int st, int64_t *b, double *x) {
+        const uint32_t d = sb + st * kStage + threadIdx.x * 16;
+        if (GI == 1) {
+            const uint4 v = lds128(d);
+            b[0] = (int32_t)v.x; b[1] = (int32_t)v.y; b[2] = (int32_t)v.z; b[3] = (int32_t)v.w;
+        } else {
+            const uint4 v = lds128(d), w = lds128(d + kGran);
+            b[0] = (int64_t)(((uint64_t)v.y << 32) | v.x); b[1] = (int64_t)(((uint64_t)v.w << 32) | v.z);
+            b[2] = (int64_t)(((uint64_t)w.y << 32) | w.x); b[3] = (int64_t)(((uint64_t)w.w << 32) | w.z);
+        }
+        const uint32_t dv = d + GI * kGran;
+        if (GV == 1) {
+            const uint4 v = lds128(dv);
+            x[0] = __uint_as_float(v.x); x[1] = __uint_as_float(v.y); x[2] = __uint_as_float(v.z); x[3] = __uint_as_float(v.w);
+        } else {
+            const uint4 v = lds128(dv), w = lds128(dv + kGran);
+            x[0] = __hiloint2double((int)v.y, (int)v.x); x[1] = __hiloint2double((int)v.w, (int)v.z);
+            x[2] = __hiloint2double((int)w.y, (int)w.x); x[3] = __hiloint2double((int)w.w, (int)w.z);
+        }
+    }
+};
 // small m: one shared-memory table per CTA.  Shared-memory atomics are native
 // only for 32-bit integer add on sm_100a (f64 and 64-bit adds compile to
 // ATOMS.CAST.SPIN.64 CAS loops, profiles/r01_ncu_full_rbi_fwd_smem_log_m1e3.txt),
@@ -350,7 +423,7 @@ __global__ void __launch_bounds__(kBThreads) rbi_fwd_log(const I *__restrict__ i
 // ATOMS.ADD returning the old value (a wrap is a carry into the high word),
 // the high word with ATOMS.ADD — exact mod 2^64.  Zero counts: 32-bit adds.
 // Merged into the global codes with RED.ADD.64.
-template <class T, class I>
+template <class T, class I, bool RING>
 __global__ void __launch_bounds__(kBThreads, kBMinBlocks) rbi_fwd_smem_log(const I *__restrict__ inds, const T *__restrict__ as,
                                                               RbiParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -368,7 +441,7 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) rbi_fwd_smem_log(const
     auto visit = [&](int64_t b, double x) {
         if ((uint64_t)b >= m) return;  // out-of-range bins (negative ones wrap): skipped (R4)
         const uint32_t o = (uint32_t)b * 4u;
-        if (x == 0.0) {
+        if ((__double_as_longlong(x) << 1) == 0) {  // +-0 (integer test, no FP64 compare)
             asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(a_zc + o) : "memory");
         } else {
             const unsigned long long q = mul_code_s(x, a_tb);
@@ -379,8 +452,38 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) rbi_fwd_smem_log(const
             asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a_hi + o), "r"(qh) : "memory");
         }
     };
-    // slab loop unrolled by two (ping-pong register buffers: no copies)
-    {
+    if constexpr (RING) {  // cp.async-staged slabs after the table (16-byte aligned streams)
+        using R = SlabRing<T, I, kRingFwd>;
+        const uint32_t sb = smem_u32(smem) + (((uint32_t)P.m * 12u + 15u) & ~15u);
+        const int64_t ns = P.n / 128;
+        const int lane = threadIdx.x & 31;
+        const int64_t ws = ((int64_t)gridDim.x * blockDim.x) >> 5;
+        const uint64_t pol = policy_evict_first();
+        const int64_t sl0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+#pragma unroll
+        for (int k = 0; k < kRingFwd; ++k) {
+            const int64_t s = sl0 + k * ws;
+            if (s < ns) R::issue(sb, k, inds, as, s * 128 + lane * 4, pol);
+            cp_async_commit();
+        }
+        int st = 0;
+        for (int64_t sl = sl0; sl < ns; sl += ws) {
+            cp_async_wait<kRingFwd - 1>();
+            int64_t b[4];
+            double x[4];
+            R::read(sb, st, b, x);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) visit(b[q], x[q]);
+            const int64_t sn = sl + kRingFwd * ws;  // refill after the values were consumed
+            if (sn < ns) R::issue(sb, st, inds, as, sn * 128 + lane * 4, pol);
+            cp_async_commit();
+            st = (st + 1 == kRingFwd) ? 0 : st + 1;
+        }
+        cp_async_wait<0>();
+        if (blockIdx.x == 0 && threadIdx.x < 32) {  // tail (< 128 elements)
+            for (int64_t e = ns * 128 + lane; e < P.n; e += 32) visit((int64_t)inds[e], (double)as[e]);
+        }
+    } else {  // slab loop unrolled by two (ping-pong register buffers: no copies)
         const int64_t ns = P.n / 128;
         const int lane = threadIdx.x & 31;
         const int64_t ws = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -457,7 +560,7 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) rbi_ext_a(const I *__r
     const int64_t R = P.cap / nw;  // this warp's region of the candidate list
     unsigned long long *reg = P.cand + 3 * gw * R;
     int64_t cnt = 0;
-    rbi_stream<T, I>(inds, as, ab, P, [&](int64_t b, double x, int64_t gi, bool ok) {
+    auto visit = [&](int64_t b, double x, int64_t gi, bool ok) {
         uint64_t k = 0;
         bool cand = false;
         if (ok) {
@@ -481,7 +584,8 @@ __global__ void __launch_bounds__(kBThreads, kBMinBlocks) rbi_ext_a(const I *__r
             }
         }
         cnt += __popc(msk);
-    });
+    };
+    rbi_stream<T, I>(inds, as, ab, P, visit);
     if (lane == 0) {
         P.ncand[1 + gw] = (unsigned long long)cnt;
         if (cnt > R) atomicOr(P.ncand, 1ull);  // overflow: phase B re-reads the inputs
@@ -931,9 +1035,24 @@ vjp_status forward(const I *inds, const T *as, T *ab, RbiParams P, cudaStream_t 
     const int64_t work = P.n / nvec + 1;
     if (OP == VJP_MUL) {
         if (sm_log <= kSmemCap) {  // small m: per-CTA shared-memory table
-            auto k = rbi_fwd_smem_log<T, I>;
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_log);
-            k<<<grid_resident(k, work, sm_log), kBThreads, sm_log, s>>>(inds, as, P);
+            const size_t sm_ring = ((sm_log + 15) & ~size_t(15)) + SlabRing<T, I, kRingFwd>::kBytes;
+            int occ_ring = 0, occ_plain = 0;  // the ring only where it keeps the occupancy
+            cudaFuncSetAttribute(rbi_fwd_smem_log<T, I, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sm_ring <= kSmemCap ? sm_ring : sm_log));
+            cudaFuncSetAttribute(rbi_fwd_smem_log<T, I, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_log);
+            if (sm_ring <= kSmemCap)
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_ring, rbi_fwd_smem_log<T, I, true>, kBThreads, sm_ring);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_plain, rbi_fwd_smem_log<T, I, false>, kBThreads, sm_log);
+            if (VJP_RING_FWD > 0 && vjph::aligned16(inds) && vjph::aligned16(as) && sm_ring <= kSmemCap &&
+                occ_ring >= occ_plain) {
+                auto k = rbi_fwd_smem_log<T, I, true>;
+                cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_ring);
+                k<<<grid_resident(k, work, sm_ring), kBThreads, sm_ring, s>>>(inds, as, P);
+            } else {
+                auto k = rbi_fwd_smem_log<T, I, false>;
+                cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_log);
+                k<<<grid_resident(k, work, sm_log), kBThreads, sm_log, s>>>(inds, as, P);
+            }
         } else {  // large m: global reductions (L2)
             rbi_fwd_log<T, I><<<grid_resident(rbi_fwd_log<T, I>, work), kBThreads, 0, s>>>(inds, as, P);
         }
@@ -943,7 +1062,7 @@ vjp_status forward(const I *inds, const T *as, T *ab, RbiParams P, cudaStream_t 
     } else {
         const size_t smk = sizeof(unsigned long long) * (size_t)P.m;
         int ga;
-        if (smk <= 128 * 1024) {
+        if (smk <= 128 * 1024) {  // (the cp.async ring measured slower here: 1.09 -> 1.20 ms, DESIGN 7.6)
             auto k = rbi_ext_a<T, I, OP, true>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smk);
             ga = grid_resident(k, work, smk);

@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(k1pData + 32, 2) scan_add_1p(const __grid_cons
     constexpr int TE = TB / (int)sizeof(T);  // tile elements
     constexpr int EPC = 16 / (int)sizeof(T); // elements per 16-byte chunk
     extern __shared__ __align__(1024) unsigned char s_raw[];
-    unsigned char *s_tile = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(s_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char *s_tile = smem_align1024(s_raw);
     __shared__ int64_t s_tick;
     __shared__ double s_wsum[NW];
     __shared__ double s_excl;

@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kLbCompute + 32, 1) scan_blocklb(const __grid_
     static_assert(PK * 8 <= kRowBytes, "the parked row must fit in the row's as_bar bytes");
 
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char *base = smem_align1024(smem_raw);
     LbSmem<Op, NT, S> &sm = *reinterpret_cast<LbSmem<Op, NT, S> *>(base + S * STG);
     const ChunkParams &p = P.c;
     const int t = threadIdx.x, warp = t >> 5;

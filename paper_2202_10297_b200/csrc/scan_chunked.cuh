@@ -34,6 +34,27 @@
 
 namespace vjpk {
 
+// Tile-data accesses of K_R / K_C: 1 = through a generic pointer (LD/ST), 0 =
+// shared-typed (LDS/STS).  The row scratch is always shared-typed.  Measured
+// (tools/time_variants.py, config 2 at 2^26 f64): MAT2 1.77 ms with shared-
+// typed tiles vs 1.68 ms generic (the generic loads are scheduled less
+// eagerly: fewer live registers around the row loops); LINREC unchanged.
+#ifndef VJP_APPLY_TILE
+#define VJP_APPLY_TILE 1
+#endif
+#ifndef VJP_REDUCE_TILE
+#define VJP_REDUCE_TILE 1
+#endif
+template <int GENERIC>
+__device__ __forceinline__ unsigned char *tile_base(unsigned char *sbase) {
+    if (GENERIC) {  // opaque to the address-space inference
+        unsigned long long r;
+        asm("mov.b64 %0, %1;" : "=l"(r) : "l"(reinterpret_cast<unsigned long long>(sbase)));
+        return reinterpret_cast<unsigned char *>(r);
+    }
+    return sbase;
+}
+
 struct ChunkParams {
     int64_t n;
     int64_t full_rows;
@@ -385,8 +406,9 @@ __global__ void __launch_bounds__(NT, 1) scan_reduce(const __grid_constant__ CUt
     static_assert(NW >= 2, "needs a forward and a reverse scan warp");
 
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    ReduceSmem<Op, NT, S> &sm = *reinterpret_cast<ReduceSmem<Op, NT, S> *>(base + S * STG);
+    unsigned char *const sbase = smem_align1024(smem_raw);
+    ReduceSmem<Op, NT, S> &sm = *reinterpret_cast<ReduceSmem<Op, NT, S> *>(sbase + S * STG);
+    unsigned char *base = tile_base<VJP_REDUCE_TILE>(sbase);
     const V yl = YL ? load_ylast<Op, T>(p.ylast) : Op::fwd_id();
 
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
@@ -487,7 +509,7 @@ __global__ void __launch_bounds__(NT, 1) scan_reduce_rs(const __grid_constant__ 
     static_assert(NW >= 2, "needs a forward and a reverse scan warp");
 
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char *base = smem_align1024(smem_raw);
     ReduceSmem<Op, NT, S> &sm = *reinterpret_cast<ReduceSmem<Op, NT, S> *>(base + S * STG);
 
     const int t = threadIdx.x, warp = t >> 5;
@@ -586,8 +608,9 @@ __global__ void __launch_bounds__(NT, 1) scan_apply(const __grid_constant__ CUte
     static_assert(NW >= 2, "needs a forward and a reverse scan warp");
 
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    ApplySmem<Op, NT, S> &sm = *reinterpret_cast<ApplySmem<Op, NT, S> *>(base + S * STG);
+    unsigned char *const sbase = smem_align1024(smem_raw);
+    ApplySmem<Op, NT, S> &sm = *reinterpret_cast<ApplySmem<Op, NT, S> *>(sbase + S * STG);
+    unsigned char *base = tile_base<VJP_APPLY_TILE>(sbase);
     const V yl = YL ? load_ylast<Op, T>(p.ylast) : Op::fwd_id();
 
     const int t = threadIdx.x, warp = t >> 5;

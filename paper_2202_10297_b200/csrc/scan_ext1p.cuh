@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(k1pData + 32, 3) scan_ext_1p(const __grid_cons
     constexpr int EPC = 16 / (int)sizeof(T);
     const Add1pParams &P = X.r;
     extern __shared__ __align__(1024) unsigned char s_raw[];
-    unsigned char *sA = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(s_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char *sA = smem_align1024(s_raw);
     unsigned char *sY = sA + TB;
     __shared__ int64_t s_tick;
     __shared__ double s_f[NW];     // warp forward aggregates

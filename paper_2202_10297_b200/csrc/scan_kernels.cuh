@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(kThreads) scan_pass1(const __grid_constant__ C
     constexpr int NB = (FWD ? 1 : 0) + (REV ? 1 : 0);
 
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char *base = smem_align1024(smem_raw);
     unsigned char *sA = base;
     unsigned char *sY = base + (FWD ? kTileBytes : 0);
     struct Small {
@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(kThreads, 2) scan_pass2(const __grid_constant_
     constexpr int NB = (FWD ? 1 : 0) + 1 + (ACC ? 1 : 0);
 
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char *base = smem_align1024(smem_raw);
     unsigned char *sA = base;
     unsigned char *sY = base + (FWD ? kTileBytes : 0);
     unsigned char *sC = sY + kTileBytes;

@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(NT + 64, (FWD || ACC) ? 2 : 3) scan_sweep(cons
     const ChunkParams &p = sp.c;
 
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char *base = smem_align1024(smem_raw);
     SweepSmem<Op, S> &ss = *reinterpret_cast<SweepSmem<Op, S> *>(base + S * STG);
 
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
