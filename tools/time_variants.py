@@ -38,6 +38,12 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
     o2 = torch.empty_like(y2)
     res["mat2_ms"] = med(lambda: vjp.scan("mat2", y2, a2, out=o2))
     del a2, y2, o2
+    am = synth.min_inputs(n, dtype=torch.float64, device="cuda")
+    ym = synth.uniform(n, 10, device="cuda")
+    om = torch.empty_like(ym)
+    for op in ("min", "max"):
+        res[f"scan_{op}_2p26_ms"] = med(lambda: vjp.scan(op, ym, am, out=om))
+    del am, ym, om
     o = torch.empty(1 << 28, dtype=torch.float64, device="cuda")
     for op in ("mul", "max"):
         inds, a, hb = synth.rbi_inputs(1 << 28, 1000, op, device="cuda")
