@@ -55,8 +55,20 @@ def main():
         for i in range(4):
             d_a[i * q:(i + 1) * q].copy_(h_in[i * q:(i + 1) * q], non_blocking=True)
 
+    def h2d_2s():  # two halves on two streams (two copy engines?)
+        cur = torch.cuda.current_stream(dev)
+        s1.wait_stream(cur)
+        s2.wait_stream(cur)
+        q = nb // 2
+        with torch.cuda.stream(s1):
+            d_a[:q].copy_(h_in[:q], non_blocking=True)
+        with torch.cuda.stream(s2):
+            d_a[q:].copy_(h_in[q:], non_blocking=True)
+        cur.wait_stream(s1)
+        cur.wait_stream(s2)
+
     for name, fn, bytes_ in (("h2d", h2d, nb), ("d2h", d2h, nb), ("h2d+d2h concurrent", both, 2 * nb),
-                             ("h2d 4 pieces", h2d4, nb)):
+                             ("h2d 4 pieces", h2d4, nb), ("h2d 2 streams", h2d_2s, nb)):
         ms = timed(fn)
         print(json.dumps({"case": name, "bytes": bytes_, "ms": ms, "GB/s": bytes_ / ms / 1e6}))
 
