@@ -2,6 +2,9 @@
 world_size 2 processes, both on cuda:0 (gpurun exposes one GPU), gloo backend
 for the tiny exchanges (dist routes them through host memory; with NCCL on an
 8-GPU box the same calls use all_gather_into_tensor / all_reduce on device).
+The NCCL data plane itself (device all_gather_into_tensor / all_reduce) runs
+in `test_dist_nccl_world1`: one rank, backend "nccl" (NCCL rejects two ranks
+on one device), the same calls and checks.
 Every rank computes its contiguous shard; rank 0 assembles and checks against
 the oracle on the whole array."""
 from __future__ import annotations
@@ -26,13 +29,15 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, backend="gloo"):
     import sys
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     try:
         import torch.distributed as dist
-        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+        if backend == "nccl":
+            torch.cuda.set_device(0)
+        dist.init_process_group(backend, init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
         import oracle
         import synth
         from paper_2202_10297_b200 import dist as vdist
@@ -139,3 +144,15 @@ def test_dist_two_ranks_one_gpu():
         p.join(timeout=60)
     for r in range(world):
         assert res[r] == "ok", res[r]
+
+
+def test_dist_nccl_world1():
+    """the same sequence with backend "nccl" at world size 1: every exchange of
+    dist.py goes through NCCL's device collectives"""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_worker, args=(0, 1, _free_port(), q, "nccl"))
+    p.start()
+    rank, res = q.get(timeout=600)
+    p.join(timeout=60)
+    assert res == "ok", res
