@@ -30,6 +30,12 @@ if len(sys.argv) > 1 and sys.argv[1] == "--child":
 
     n = 1 << 26
     res = {"build": name}
+    if os.environ.get("TV_SCAN_ADD"):
+        for dt in (torch.float64, torch.float32):
+            yb = synth.scan_add_seed(1 << 30, device="cuda").to(dt)
+            ob = torch.empty_like(yb)
+            res[f"scan_add_2p30_{str(dt)[-7:]}_ms"] = med(lambda: vjp.scan("add", yb, out=ob))
+            del yb, ob
     a1, y1 = synth.linrec_inputs(n, device="cuda")
     o1 = torch.empty_like(y1)
     res["linrec_ms"] = med(lambda: vjp.scan("linrec", y1, a1, out=o1))
